@@ -1,0 +1,66 @@
+// Internal declarations shared by the CUDA translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/hespmm_b200.h"
+#include "modarith.cuh"
+
+namespace hs {
+
+// Kernel-side view of a context (passed by value).
+struct Dev {
+    u32 n;
+    int log_n;
+    int L;                       // chain has L+1 primes; aux prime index L+1
+    u64 aux_q;                   // the key-switch auxiliary prime p
+    const PrimeConst* pc;        // [L+2]
+    const ulonglong2* tw;        // [(L+2) * n] {w, floor(w 2^64 / q)} forward roots
+    const ulonglong2* itw;       // inverse roots
+    const ulonglong2* df;        // [L+1] digit factor (Q_L/q_i)^-1 mod q_i, Shoup pair
+    const ulonglong2* auxinv;    // [L+1] p^-1 mod q_m
+    const ulonglong2* qlinv;     // [(L+1)*(L+1)] q_lvl^-1 mod q_i at [lvl*(L+1)+i]
+};
+
+void set_error(const std::string& msg);
+
+// Number of kernels this library has launched (for the bench's gpu_launches).
+void note_launch(int count = 1);
+
+struct KeyBuf {
+    u64* d = nullptr;            // [2][L+1][L+2][n], Montgomery form
+};
+
+}  // namespace hs
+
+// Opaque context type of the C-ABI.
+struct hs_ctx {
+    int device = 0;
+    hs::Dev dev{};
+    u32 n = 0;
+    int log_n = 0;
+    int L = 0;
+    std::vector<u64> primes;                 // chain then aux
+    std::vector<PrimeConst> pc;              // host copy
+    std::vector<u64> df, auxinv;             // host copies (plain values)
+    std::vector<u64> qlinv;                  // [(L+1)*(L+1)]
+    void* d_blob = nullptr;                  // one allocation for all tables
+    hs::KeyBuf relin;
+    size_t batch_bytes = (size_t)6 << 30;   // runner work-buffer budget
+    std::unordered_map<u32, hs::KeyBuf> galois;   // normalised step -> key
+    size_t key_bytes() const { return (size_t)2 * (L + 1) * (L + 2) * n * sizeof(u64); }
+};
+
+#define HS_CUDA(call)                                                          \
+    do {                                                                       \
+        cudaError_t e_ = (call);                                               \
+        if (e_ != cudaSuccess) {                                               \
+            hs::set_error(std::string("CUDA error: ") + cudaGetErrorString(e_) + \
+                          " at " __FILE__ ":" + std::to_string(__LINE__));      \
+            return e_ == cudaErrorMemoryAllocation ? HS_OUT_OF_MEMORY           \
+                                                   : HS_CUDA_ERROR;            \
+        }                                                                      \
+    } while (0)

@@ -1,0 +1,616 @@
+// Device operations of the encrypted SpMSpM path: limb kernels, key
+// switching (decompose -> ModUp -> key inner product -> ModDown), rescale,
+// tensor product, NTT-domain Galois automorphism, accumulation.
+//
+// Reference semantics (paths relative to /root/reference/pkg/src/hespmm/):
+//   key switch     ckks/context.py:462-498
+//   relinearize    ckks/context.py:363-380 (+ _digits_from_ntt :454-460)
+//   rescale        ckks/context.py:382-399
+//   eval_rotate    ckks/context.py:401-452
+//   mult_ct / pt   ckks/context.py:334-361
+// Every kernel writes canonical residues, so results are bit-identical to
+// the reference regardless of the (lazy) reduction strategy used inside.
+#include "ops.cuh"
+
+#include <atomic>
+
+namespace hs {
+
+static std::atomic<long long> g_launches{0};
+void note_launch(int count) { g_launches += count; }
+long long launch_count() { return g_launches.load(); }
+
+// =========================================================== helpers
+
+HS_DEV u64 canon4(u64 v, const PrimeConst& P) {    // [0,4q) -> [0,q)
+    return csub(csub(v, P.two_q), P.q);
+}
+
+// 128-bit multiply-accumulate (hi:lo) += a*b.
+HS_DEV void mac128(u64& lo, u64& hi, u64 a, u64 b) {
+    asm("mad.lo.cc.u64 %0, %2, %3, %0;\n\t"
+        "madc.hi.u64 %1, %2, %3, %1;"
+        : "+l"(lo), "+l"(hi)
+        : "l"(a), "l"(b));
+}
+
+// Montgomery reduction of a 128-bit accumulator: returns X * 2^-64 mod q.
+HS_DEV u64 redc128(u64 lo, u64 hi, const PrimeConst& P) {
+    hi = reduce64(hi, P);                    // X' = (hi mod q) 2^64 + lo < q 2^64
+    u64 m = lo * P.qinv_neg;
+    u64 r = hi + mulhi64(m, P.q) + (lo != 0ull);
+    return csub(r, P.q);
+}
+
+// Barrett reduction of a 128-bit value x < 2 q^2 (same estimate as mul_mod).
+HS_DEV u64 barrett128(u64 lo, u64 hi, const PrimeConst& P) {
+    u64 q1 = (hi << (65 - P.k)) | (lo >> (P.k - 1));
+    u64 qt = mulhi64(q1, P.mu64);
+    u64 r = lo - qt * P.q;
+    r = csub(r, P.two_q);
+    r = csub(r, P.q);
+    return csub(r, P.q);
+}
+
+// NTT-domain Galois automorphism X -> X^g: out[k] = in[perm(k)].
+// Slot k of a limb holds a(psi^(2 brev(k) + 1)) (bit-reversed output order of
+// the reference NTT), so out[k] = in[k'] with 2 brev(k') + 1 = (2 brev(k) + 1) g
+// mod 2n.  Pure index map, no sign flips; equals the reference's
+// INTT -> signed coefficient permutation -> NTT (context.py:416-452).
+HS_DEV u32 galois_perm(u32 k, u32 g, int log_n) {
+    u32 br = __brev(k) >> (32 - log_n);
+    u32 e = (u32)((((u64)(2 * br + 1)) * g) & ((2ull << log_n) - 1));
+    return __brev((e - 1) >> 1) >> (32 - log_n);
+}
+
+// =========================================================== plain NTT jobs
+
+template <bool FWD>
+struct JobPlain {
+    u64* buf;           // [jobs][n], in place
+    const u64* src;     // optional separate source (same layout) or nullptr
+    PrimeMap pm;
+    u32 n;
+    HS_DEV int prime(int jb) const { return pm.p[jb % pm.nl]; }
+    HS_DEV u64 load(int jb, u32 j, const PrimeConst&) const {
+        return (src ? src : buf)[(size_t)jb * n + j];
+    }
+    HS_DEV u64* scratch(int jb) const { return buf + (size_t)jb * n; }
+    HS_DEV void store(int jb, u32 j, u64 v, const PrimeConst& P) const {
+        buf[(size_t)jb * n + j] = FWD ? canon4(v, P) : shoup(v, P.n_inv, P.n_inv_sh, P.q);
+    }
+};
+
+void ntt_plain(const Dev& d, u64* buf, const u64* src, int njobs, const PrimeMap& pm, bool fwd,
+               cudaStream_t st) {
+    if (fwd) launch_ntt<true>(d, JobPlain<true>{buf, src, pm, d.n}, njobs, st);
+    else launch_ntt<false>(d, JobPlain<false>{buf, src, pm, d.n}, njobs, st);
+}
+
+// Inverse NTT of limb `limb` of each item of an ItemPtr set, written to dst.
+// Item jb = b*npoly + poly reads ptr(b) + (poly*nl + limb)*n.
+struct JobInvGather {
+    ItemPtr in;
+    int npoly, nl, limb, prime_idx;
+    u64* dst;           // [jobs][n]
+    u32 n;
+    HS_DEV int prime(int) const { return prime_idx; }
+    HS_DEV u64 load(int jb, u32 j, const PrimeConst&) const {
+        int b = jb / npoly, poly = jb % npoly;
+        return in.at(b)[((size_t)poly * nl + limb) * n + j];
+    }
+    HS_DEV u64* scratch(int jb) const { return dst + (size_t)jb * n; }
+    HS_DEV void store(int jb, u32 j, u64 v, const PrimeConst& P) const {
+        dst[(size_t)jb * n + j] = shoup(v, P.n_inv, P.n_inv_sh, P.q);
+    }
+};
+
+// =========================================================== key switching
+// Work buffers for a batch of B items at level l (all compact):
+//   E   [B][l+1][l+2][n]  ModUp output, NTT domain; slot l+1 is the aux prime;
+//                         slot i of digit i holds x_i * df_i (never lifted).
+//   D   [B][l+1][n]       digits in coefficient domain.
+//   ACC [B][2][l+2][n]    key inner products (b then a component).
+//   T   [B][2][n]         INTT of ACC aux limbs.
+
+// Digit sources: the NTT-domain limb x_i that is decomposed.
+struct SrcPlain {      // x = ct(b).c1[i]   (relin of a stored d2 uses poly_off 2)
+    ItemPtr ct;
+    int poly;          // which poly holds x
+    HS_DEV u64 x(int b, int i, int l, u32 j, u32 n, const Dev&, const PrimeConst&) const {
+        return ct.at(b)[((size_t)poly * (l + 1) + i) * n + j];
+    }
+};
+struct SrcPerm {       // x = automorphism_g(ct(b).c1)[i]
+    ItemPtr ct;
+    const u32* gal;    // per item Galois element
+    HS_DEV u64 x(int b, int i, int l, u32 j, u32 n, const Dev& d, const PrimeConst&) const {
+        return ct.at(b)[((size_t)(l + 1) + i) * n + galois_perm(j, gal[b], d.log_n)];
+    }
+};
+struct SrcTensor {     // x = d2 = a1 * b1 of the tensor product of two cts
+    ItemPtr a, bb;
+    HS_DEV u64 x(int b, int i, int l, u32 j, u32 n, const Dev&, const PrimeConst& P) const {
+        size_t o = ((size_t)(l + 1) + i) * n + j;
+        return mul_mod(a.at(b)[o], bb.at(b)[o], P);
+    }
+};
+
+template <class Src>
+struct JobDecompose {                       // inverse NTT, job = b*(l+1)+i
+    Src src;
+    u64* E;
+    u64* D;
+    const ulonglong2* df;
+    int l;
+    u32 n;
+    Dev d;
+    HS_DEV int prime(int jb) const { return jb % (l + 1); }
+    HS_DEV u64 load(int jb, u32 j, const PrimeConst& P) const {
+        int b = jb / (l + 1), i = jb % (l + 1);
+        u64 x = src.x(b, i, l, j, n, d, P);
+        ulonglong2 w = df[i];
+        u64 v = shoup(x, w.x, w.y, P.q);
+        E[((size_t)jb * (l + 2) + i) * n + j] = v;
+        return v;
+    }
+    HS_DEV u64* scratch(int jb) const { return D + (size_t)jb * n; }
+    HS_DEV void store(int jb, u32 j, u64 v, const PrimeConst& P) const {
+        D[(size_t)jb * n + j] = shoup(v, P.n_inv, P.n_inv_sh, P.q);
+    }
+};
+
+struct JobModUp {                           // forward NTT, job = (b*(l+1)+i)*(l+1)+t
+    const u64* D;
+    u64* E;
+    int l, L;
+    u32 n;
+    const PrimeConst* pc;
+    HS_DEV void decode(int jb, int& bi, int& i, int& m) const {
+        int t = jb % (l + 1);
+        bi = jb / (l + 1);
+        i = bi % (l + 1);
+        m = t < i ? t : t + 1;              // m in [0, l+1] \ {i}; l+1 = aux
+    }
+    HS_DEV int prime(int jb) const {
+        int bi, i, m;
+        decode(jb, bi, i, m);
+        return m <= l ? m : L + 1;
+    }
+    HS_DEV u64 load(int jb, u32 j, const PrimeConst& P) const {
+        int bi, i, m;
+        decode(jb, bi, i, m);
+        return lift_mod(D[(size_t)bi * n + j], pc[i].q, P);
+    }
+    HS_DEV u64* scratch(int jb) const {
+        int bi, i, m;
+        decode(jb, bi, i, m);
+        return E + ((size_t)bi * (l + 2) + m) * n;
+    }
+    HS_DEV void store(int jb, u32 j, u64 v, const PrimeConst& P) const {
+        scratch(jb)[j] = canon4(v, P);
+    }
+};
+
+// Key inner product: ACC[b][c][m] = sum_i E[b][i][m][perm(k)] * K_b[c][i][m].
+// Keys are stored in Montgomery form, so one REDC of the 128-bit sum yields
+// the plain residue.  grid = (n/256, l+2, B).
+__global__ void __launch_bounds__(256)
+ks_inner_kernel(Dev d, int l, const u64* __restrict__ E, size_t e_item_stride,
+                const u64* const* __restrict__ keys, const u32* __restrict__ gal,
+                u64* __restrict__ ACC) {
+    const u32 n = d.n;
+    const u32 k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int m = blockIdx.y;
+    const int b = blockIdx.z;
+    if (k >= n) return;
+    const int pm = m <= l ? m : d.L + 1;
+    const PrimeConst P = d.pc[pm];
+    const u32 g = gal ? gal[b] : 0u;
+    const u32 src = g ? galois_perm(k, g, d.log_n) : k;
+    const u64* Eb = E + (size_t)b * e_item_stride;
+    const u64* key = keys[b];
+    const size_t kstride = (size_t)(d.L + 2) * n;                  // one digit
+    const u64* kb = key + (size_t)pm * n + k;
+    const u64* ka = key + (size_t)(d.L + 1) * kstride + (size_t)pm * n + k;
+    u64 lb = 0, hb = 0, la = 0, ha = 0;
+    for (int i = 0; i <= l; i++) {
+        const u64 e = Eb[((size_t)i * (l + 2) + m) * n + src];
+        mac128(lb, hb, e, kb[(size_t)i * kstride]);
+        mac128(la, ha, e, ka[(size_t)i * kstride]);
+    }
+    u64* out = ACC + (size_t)b * 2 * (l + 2) * n;
+    out[(size_t)m * n + k] = redc128(lb, hb, P);
+    out[((size_t)(l + 2) + m) * n + k] = redc128(la, ha, P);
+}
+
+// ModDown addends (what is added to the key-switch output).
+struct AddNone {
+    HS_DEV u64 v(int, int, int, int, u32, const Dev&, const PrimeConst&) const { return 0; }
+};
+struct AddTensor {     // relinearize after mult_ct: d0 = a0 b0, d1 = a0 b1 + a1 b0
+    ItemPtr a, bb;
+    HS_DEV u64 v(int b, int poly, int m, int l, u32 j, const Dev& d, const PrimeConst& P) const {
+        const size_t n = d.n;
+        const u64* A = a.at(b);
+        const u64* B = bb.at(b);
+        const u64 a0 = A[m * n + j], b0 = B[m * n + j];
+        if (poly == 0) return mul_mod(a0, b0, P);
+        const u64 a1 = A[((size_t)(l + 1) + m) * n + j], b1 = B[((size_t)(l + 1) + m) * n + j];
+        u64 lo = 0, hi = 0;
+        mac128(lo, hi, a0, b1);
+        mac128(lo, hi, a1, b0);
+        return barrett128(lo, hi, P);
+    }
+};
+struct AddPoly {       // d0/d1 taken from a stored ct (npoly polys at level l)
+    ItemPtr ct;
+    HS_DEV u64 v(int b, int poly, int m, int l, u32 j, const Dev& d, const PrimeConst&) const {
+        return ct.at(b)[((size_t)poly * (l + 1) + m) * d.n + j];
+    }
+};
+struct AddPermC0 {     // rotation: automorphism_g(c0) on poly 0
+    ItemPtr ct;
+    const u32* gal;
+    HS_DEV u64 v(int b, int poly, int m, int l, u32 j, const Dev& d, const PrimeConst&) const {
+        if (poly) return 0;
+        return ct.at(b)[(size_t)m * d.n + galois_perm(j, gal[b], d.log_n)];
+    }
+};
+
+template <class Add>
+struct JobModDown {                          // forward NTT, job = (b*2+c)*(l+1)+m
+    const u64* T;
+    const u64* ACC;
+    ItemPtr out;                             // per item ct [2][l+1][n]
+    Add add;
+    int l;
+    Dev d;
+    HS_DEV int prime(int jb) const { return jb % (l + 1); }
+    HS_DEV u64 load(int jb, u32 j, const PrimeConst& P) const {
+        return lift_mod(T[(size_t)(jb / (l + 1)) * d.n + j], d.aux_q, P);
+    }
+    HS_DEV u64* scratch(int jb) const {
+        int bc = jb / (l + 1), m = jb % (l + 1);
+        return out.atw(bc >> 1) + ((size_t)(bc & 1) * (l + 1) + m) * d.n;
+    }
+    HS_DEV void store(int jb, u32 j, u64 v, const PrimeConst& P) const {
+        int bc = jb / (l + 1), m = jb % (l + 1);
+        u64 acc = ACC[((size_t)bc * (l + 2) + m) * d.n + j];
+        ulonglong2 w = d.auxinv[m];
+        u64 r = shoup(sub_mod(acc, canon4(v, P), P.q), w.x, w.y, P.q);
+        r = add_mod(r, add.v(bc >> 1, bc & 1, m, l, j, d, P), P.q);
+        scratch(jb)[j] = r;
+    }
+};
+
+size_t ks_scratch_elems(int B, int l, u32 n) {
+    return (size_t)B * n * ((size_t)(l + 1) * (l + 2) + (l + 1) + 2 * (l + 2) + 2);
+}
+
+size_t ks_hoisted_scratch_elems(int R, int l, u32 n) {
+    return (size_t)n * ((size_t)(l + 1) * (l + 2) + (l + 1) + (size_t)R * (2 * (l + 2) + 2));
+}
+
+// ModDown of ACC (B items) into out with addend.
+template <class Add>
+static void mod_down(const Dev& d, int B, int l, const u64* ACC, u64* T, const Add& add,
+                     ItemPtr out, cudaStream_t st) {
+    launch_ntt<false>(d, JobInvGather{strided(ACC, (size_t)(l + 2) * d.n), 1, l + 2, l + 1,
+                                      d.L + 1, T, d.n},
+                      B * 2, st);
+    launch_ntt<true>(d, JobModDown<Add>{T, ACC, out, add, l, d}, B * 2 * (l + 1), st);
+}
+
+template <class Src, class Add>
+static void key_switch_batch(const Dev& d, int B, int l, const Src& src, const Add& add,
+                             const u64* const* keys, ItemPtr out, u64* scratch, cudaStream_t st) {
+    const u32 n = d.n;
+    u64* E = scratch;
+    u64* D = E + (size_t)B * (l + 1) * (l + 2) * n;
+    u64* ACC = D + (size_t)B * (l + 1) * n;
+    u64* T = ACC + (size_t)B * 2 * (l + 2) * n;
+    launch_ntt<false>(d, JobDecompose<Src>{src, E, D, d.df, l, n, d}, B * (l + 1), st);
+    launch_ntt<true>(d, JobModUp{D, E, l, d.L, n, d.pc}, B * (l + 1) * (l + 1), st);
+    dim3 g((n + 255) / 256, l + 2, B);
+    ks_inner_kernel<<<g, 256, 0, st>>>(d, l, E, (size_t)(l + 1) * (l + 2) * n, keys, nullptr, ACC);
+    note_launch();
+    mod_down(d, B, l, ACC, T, add, out, st);
+}
+
+void relin_batch(const Dev& d, int B, int l, ItemPtr ct3, const u64* const* keys, ItemPtr out,
+                 u64* scratch, cudaStream_t st) {
+    key_switch_batch(d, B, l, SrcPlain{ct3, 2}, AddPoly{ct3}, keys, out, scratch, st);
+}
+
+void mult_relin_batch(const Dev& d, int B, int l, ItemPtr a, ItemPtr b, const u64* const* keys,
+                      ItemPtr out, u64* scratch, cudaStream_t st) {
+    key_switch_batch(d, B, l, SrcTensor{a, b}, AddTensor{a, b}, keys, out, scratch, st);
+}
+
+void rotate_batch(const Dev& d, int B, int l, ItemPtr ct, const u32* gal, const u64* const* keys,
+                  ItemPtr out, u64* scratch, cudaStream_t st) {
+    key_switch_batch(d, B, l, SrcPerm{ct, gal}, AddPermC0{ct, gal}, keys, out, scratch, st);
+}
+
+// Hoisted rotations (P3 of SURVEY.md): decompose + ModUp the source once; per
+// step only the automorphism-gathered inner product and ModDown remain.
+void rotate_hoisted(const Dev& d, int R, int l, const u64* src, const u32* gal,
+                    const u64* const* keys, ItemPtr out, u64* scratch, cudaStream_t st) {
+    const u32 n = d.n;
+    u64* E = scratch;
+    u64* D = E + (size_t)(l + 1) * (l + 2) * n;
+    u64* ACC = D + (size_t)(l + 1) * n;
+    u64* T = ACC + (size_t)R * 2 * (l + 2) * n;
+    ItemPtr s = strided(src, 0);
+    launch_ntt<false>(d, JobDecompose<SrcPlain>{SrcPlain{s, 1}, E, D, d.df, l, n, d}, l + 1, st);
+    launch_ntt<true>(d, JobModUp{D, E, l, d.L, n, d.pc}, (l + 1) * (l + 1), st);
+    dim3 g((n + 255) / 256, l + 2, R);
+    ks_inner_kernel<<<g, 256, 0, st>>>(d, l, E, 0, keys, gal, ACC);
+    note_launch();
+    mod_down(d, R, l, ACC, T, AddPermC0{s, gal}, out, st);
+}
+
+// =========================================================== rescale
+
+struct JobRescale {                          // forward NTT, job = (b*npoly+c)*l+i
+    const u64* T;
+    ItemPtr in, out, mask;
+    int l, npoly;
+    const PrimeConst* pc;
+    const ulonglong2* qlinv;                 // row for level l
+    u32 n;
+    HS_DEV int prime(int jb) const { return jb % l; }
+    HS_DEV u64 load(int jb, u32 j, const PrimeConst& P) const {
+        return lift_mod(T[(size_t)(jb / l) * n + j], pc[l].q, P);
+    }
+    HS_DEV u64* scratch(int jb) const {
+        int bc = jb / l, i = jb % l;
+        return out.atw(bc / npoly) + ((size_t)(bc % npoly) * l + i) * n;
+    }
+    HS_DEV void store(int jb, u32 j, u64 v, const PrimeConst& P) const {
+        int bc = jb / l, i = jb % l;
+        int b = bc / npoly, c = bc % npoly;
+        u64 x = in.at(b)[((size_t)c * (l + 1) + i) * n + j];
+        ulonglong2 w = qlinv[i];
+        u64 r = shoup(sub_mod(x, canon4(v, P), P.q), w.x, w.y, P.q);
+        if (mask.tab || mask.base) r = mont_mul(r, mask.at(b)[(size_t)i * n + j], P.q, P.qinv_neg);
+        scratch(jb)[j] = r;
+    }
+};
+
+size_t rescale_scratch_elems(int B, int npoly, u32 n) { return (size_t)B * npoly * n; }
+
+void rescale_batch(const Dev& d, int B, int l, int npoly, ItemPtr in, ItemPtr out,
+                   ItemPtr mask_mont, u64* T, cudaStream_t st) {
+    launch_ntt<false>(d, JobInvGather{in, npoly, l + 1, l, l, T, d.n}, B * npoly, st);
+    JobRescale jr{T, in, out, mask_mont, l, npoly, d.pc, d.qlinv + (size_t)l * (d.L + 1), d.n};
+    launch_ntt<true>(d, jr, B * npoly * l, st);
+}
+
+// =========================================================== elementwise
+
+__global__ void tensor_kernel(Dev d, int l, ItemPtr a, ItemPtr b, ItemPtr out) {
+    const u32 n = d.n;
+    const u32 k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y, it = blockIdx.z;
+    if (k >= n) return;
+    const PrimeConst P = d.pc[i];
+    const size_t nl = l + 1;
+    const u64* A = a.at(it);
+    const u64* B = b.at(it);
+    u64* O = out.atw(it);
+    const u64 a0 = A[i * n + k], a1 = A[(nl + i) * n + k];
+    const u64 b0 = B[i * n + k], b1 = B[(nl + i) * n + k];
+    O[i * n + k] = mul_mod(a0, b0, P);
+    u64 lo = 0, hi = 0;
+    mac128(lo, hi, a0, b1);
+    mac128(lo, hi, a1, b0);
+    O[(nl + i) * n + k] = barrett128(lo, hi, P);
+    O[(2 * nl + i) * n + k] = mul_mod(a1, b1, P);
+}
+
+void tensor_batch(const Dev& d, int B, int l, ItemPtr a, ItemPtr b, ItemPtr out, cudaStream_t st) {
+    dim3 g((d.n + 255) / 256, l + 1, B);
+    tensor_kernel<<<g, 256, 0, st>>>(d, l, a, b, out);
+    note_launch();
+}
+
+__global__ void mult_pt_kernel(Dev d, int l, int npoly, ItemPtr ct, ItemPtr pt, ItemPtr out,
+                               bool mont) {
+    const u32 n = d.n;
+    const u32 k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y % (l + 1), c = blockIdx.y / (l + 1), it = blockIdx.z;
+    if (k >= n) return;
+    const PrimeConst P = d.pc[i];
+    const size_t o = ((size_t)c * (l + 1) + i) * n + k;
+    const u64 x = ct.at(it)[o], y = pt.at(it)[(size_t)i * n + k];
+    out.atw(it)[o] = mont ? mont_mul(x, y, P.q, P.qinv_neg) : mul_mod(x, y, P);
+}
+
+void mult_pt_batch(const Dev& d, int B, int l, int npoly, ItemPtr ct, ItemPtr pt, ItemPtr out,
+                   bool pt_mont, cudaStream_t st) {
+    dim3 g((d.n + 255) / 256, npoly * (l + 1), B);
+    mult_pt_kernel<<<g, 256, 0, st>>>(d, l, npoly, ct, pt, out, pt_mont);
+    note_launch();
+}
+
+__global__ void add_kernel(Dev d, int l, ItemPtr a, ItemPtr b, ItemPtr out) {
+    const u32 n = d.n;
+    const u32 k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y % (l + 1), it = blockIdx.z;
+    if (k >= n) return;
+    const size_t o = (size_t)blockIdx.y * n + k;
+    out.atw(it)[o] = add_mod(a.at(it)[o], b.at(it)[o], d.pc[i].q);
+}
+
+void add_batch(const Dev& d, int B, int l, int npoly, ItemPtr a, ItemPtr b, ItemPtr out,
+               cudaStream_t st) {
+    dim3 g((d.n + 255) / 256, npoly * (l + 1), B);
+    add_kernel<<<g, 256, 0, st>>>(d, l, a, b, out);
+    note_launch();
+}
+
+__global__ void accum_kernel(Dev d, int B, int nl, ItemPtr src, u64* acc) {
+    const u32 n = d.n;
+    const u32 k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int m = blockIdx.y % nl;
+    const u64 q = d.pc[m].q;
+    const size_t o = (size_t)blockIdx.y * n + k;
+    u64 s = acc[o];
+    for (int b = 0; b < B; b++) s = add_mod(s, src.at(b)[o], q);
+    acc[o] = s;
+}
+
+void accumulate(const Dev& d, int B, int nl, int npoly, ItemPtr src, u64* acc, cudaStream_t st) {
+    if (B <= 0) return;
+    dim3 g((d.n + 255) / 256, npoly * nl);
+    accum_kernel<<<g, 256, 0, st>>>(d, B, nl, src, acc);
+    note_launch();
+}
+
+__global__ void mont_kernel(Dev d, u64* buf, size_t total, PrimeMap pm, bool inverse) {
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= total) return;
+    const int limb = (int)((idx / d.n) % pm.nl);
+    const PrimeConst P = d.pc[pm.p[limb]];
+    buf[idx] = mont_mul(buf[idx], inverse ? 1ull : P.r2_mod, P.q, P.qinv_neg);
+}
+
+void to_montgomery(const Dev& d, u64* buf, size_t nlimb_total, const PrimeMap& pm, bool inverse,
+                   cudaStream_t st) {
+    size_t total = nlimb_total * d.n;
+    if (!total) return;
+    mont_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(d, buf, total, pm, inverse);
+    note_launch();
+}
+
+__global__ void signed_kernel(Dev d, const long long* coeffs, int nl, PrimeMap pm, u64* out) {
+    const u32 k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= d.n) return;
+    const int l = blockIdx.y;
+    const PrimeConst P = d.pc[pm.p[l]];
+    const long long c = coeffs[k];
+    u64 r;
+    if (c >= 0) {
+        r = reduce64((u64)c, P);
+    } else {
+        u64 t = reduce64((u64)(-(c + 1)) + 1ull, P);
+        r = t ? P.q - t : 0ull;
+    }
+    out[(size_t)l * d.n + k] = r;
+}
+
+void signed_to_limbs(const Dev& d, const long long* coeffs, int nl, const PrimeMap& pm, u64* out,
+                     cudaStream_t st) {
+    dim3 g((d.n + 255) / 256, nl);
+    signed_kernel<<<g, 256, 0, st>>>(d, coeffs, nl, pm, out);
+    note_launch();
+}
+
+// key layout [2][L+1][L+2][n]; ntt_e [L+1][L+2][n]; target/sk [L+2][n]; f [(L+1)*(L+1)]
+__global__ void ksk_kernel(Dev d, u64* key, const u64* ntt_e, const u64* target, const u64* sk,
+                           const ulonglong2* f) {
+    const u32 n = d.n;
+    const u32 k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int m = blockIdx.y, i = blockIdx.z, L = d.L;
+    const PrimeConst P = d.pc[m];
+    const size_t o = ((size_t)i * (L + 2) + m) * n + k;
+    u64 acc = ntt_e[o];
+    if (m <= L) {
+        ulonglong2 w = f[i * (L + 1) + m];
+        acc = add_mod(acc, shoup(target[(size_t)m * n + k], w.x, w.y, P.q), P.q);
+    }
+    const u64* a = key + (size_t)(L + 1) * (L + 2) * n;
+    acc = sub_mod(acc, mul_mod(a[o], sk[(size_t)m * n + k], P), P.q);
+    key[o] = acc;
+}
+
+void ksk_combine(const Dev& d, u64* key, const u64* ntt_e, const u64* target, const u64* sk,
+                 const ulonglong2* f, cudaStream_t st) {
+    dim3 g((d.n + 255) / 256, d.L + 2, d.L + 1);
+    ksk_kernel<<<g, 256, 0, st>>>(d, key, ntt_e, target, sk, f);
+    note_launch();
+}
+
+__global__ void enc_kernel(Dev d, int nl, const u64* v, const u64* pkb, const u64* pka,
+                           const u64* e0, const u64* e1, const u64* pt, u64* ct) {
+    const u32 n = d.n;
+    const u32 k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int i = blockIdx.y;
+    const PrimeConst P = d.pc[i];
+    const size_t o = (size_t)i * n + k;
+    const u64 vv = v[o];
+    u64 c0 = add_mod(mul_mod(vv, pkb[o], P), e0[o], P.q);
+    ct[o] = add_mod(c0, pt[o], P.q);
+    ct[(size_t)nl * n + o] = add_mod(mul_mod(vv, pka[o], P), e1[o], P.q);
+}
+
+void encrypt_combine(const Dev& d, int nl, const u64* v, const u64* pkb, const u64* pka,
+                     const u64* e0, const u64* e1, const u64* pt, u64* ct, cudaStream_t st) {
+    dim3 g((d.n + 255) / 256, nl);
+    enc_kernel<<<g, 256, 0, st>>>(d, nl, v, pkb, pka, e0, e1, pt, ct);
+    note_launch();
+}
+
+__global__ void dec_kernel(Dev d, int nl, const u64* ct, const u64* sk, u64* pt) {
+    const u32 n = d.n;
+    const u32 k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int i = blockIdx.y;
+    const PrimeConst P = d.pc[i];
+    const size_t o = (size_t)i * n + k;
+    pt[o] = add_mod(ct[o], mul_mod(ct[(size_t)nl * n + o], sk[o], P), P.q);
+}
+
+void decrypt_combine(const Dev& d, int nl, const u64* ct, const u64* sk, u64* pt, cudaStream_t st) {
+    dim3 g((d.n + 255) / 256, nl);
+    dec_kernel<<<g, 256, 0, st>>>(d, nl, ct, sk, pt);
+    note_launch();
+}
+
+__global__ void seam_kernel(int op, size_t count, const u64* a, const u64* b, u64* out,
+                            PrimeConst P, u64 s, u64 s_sh, u64 q_src) {
+    const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= count) return;
+    const u64 q = P.q;
+    switch (op) {
+        case SEAM_ADD: out[k] = add_mod(a[k], b[k], q); break;
+        case SEAM_SUB: out[k] = sub_mod(a[k], b[k], q); break;
+        case SEAM_NEG: out[k] = a[k] ? q - a[k] : 0ull; break;
+        case SEAM_MUL: out[k] = mul_mod(a[k], b[k], P); break;
+        case SEAM_SCALAR: out[k] = shoup(a[k], s, s_sh, q); break;
+        case SEAM_FMA: out[k] = add_mod(out[k], mul_mod(a[k], b[k], P), q); break;
+        case SEAM_EXTEND: out[k] = lift_mod(a[k], q_src, P); break;
+    }
+}
+
+void seam_op(int op, size_t count, const u64* a, const u64* b, u64* out, PrimeConst P, u64 s,
+             u64 q_src, cudaStream_t st) {
+    if (!count) return;
+    s %= P.q;
+    u64 s_sh = (u64)(((unsigned __int128)s << 64) / P.q);
+    seam_kernel<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(op, count, a, b, out, P, s, s_sh,
+                                                                 q_src);
+    note_launch();
+}
+
+}  // namespace hs
+
+namespace hs {
+__global__ void reduce_kernel(Dev d, u64* data, int nl) {
+    const u32 k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= d.n) return;
+    const PrimeConst P = d.pc[blockIdx.y % nl];
+    const size_t o = (size_t)blockIdx.y * d.n + k;
+    data[o] = reduce64(data[o], P);
+}
+void reduce_mod(const Dev& d, u64* data, int npoly, int nl, cudaStream_t st) {
+    dim3 g((d.n + 255) / 256, npoly * nl);
+    reduce_kernel<<<g, 256, 0, st>>>(d, data, nl);
+    note_launch();
+}
+}  // namespace hs

@@ -1,0 +1,91 @@
+// Declarations of the device operations (ops.cu) used by the C-ABI layer.
+#pragma once
+#include "ntt.cuh"
+
+namespace hs {
+
+// Limb index within an item -> prime index.
+struct PrimeMap {
+    unsigned char p[64];
+    int nl;
+};
+
+// Per-item pointer: table of pointers, or base + b * stride.
+struct ItemPtr {
+    const u64* const* tab;
+    const u64* base;
+    size_t stride;
+    HS_DEV const u64* at(int b) const { return tab ? tab[b] : base + (size_t)b * stride; }
+    HS_DEV u64* atw(int b) const { return const_cast<u64*>(at(b)); }
+};
+
+inline ItemPtr strided(const u64* base, size_t stride) { return ItemPtr{nullptr, base, stride}; }
+inline ItemPtr table(const u64* const* tab) { return ItemPtr{tab, nullptr, 0}; }
+
+PrimeConst make_prime_const(u64 q, u32 n);
+long long launch_count();
+inline PrimeMap prime_map_range(int first, int count) {
+    PrimeMap m{};
+    m.nl = count;
+    for (int i = 0; i < count && i < 64; i++) m.p[i] = (unsigned char)(first + i);
+    return m;
+}
+
+// ---- batched transforms
+void ntt_plain(const Dev& d, u64* buf, const u64* src, int njobs, const PrimeMap& pm, bool fwd,
+               cudaStream_t st);
+
+// ---- key switching
+// Scratch (u64 elements) needed by key_switch_* for B items at level l.
+size_t ks_scratch_elems(int B, int l, u32 n);
+size_t ks_hoisted_scratch_elems(int R, int l, u32 n);
+
+// Relinearize B degree-2 cts stored as [3][l+1][n] (ItemPtr ct3) -> out [2][l+1][n].
+void relin_batch(const Dev& d, int B, int l, ItemPtr ct3, const u64* const* keys, ItemPtr out,
+                 u64* scratch, cudaStream_t st);
+// mult_ct fused with relinearize: out = relin(a (x) b) for B pairs at level l.
+void mult_relin_batch(const Dev& d, int B, int l, ItemPtr a, ItemPtr b, const u64* const* keys,
+                      ItemPtr out, u64* scratch, cudaStream_t st);
+// Rotation of B cts at level l by Galois elements gal[b] with keys[b].
+void rotate_batch(const Dev& d, int B, int l, ItemPtr ct, const u32* gal, const u64* const* keys,
+                  ItemPtr out, u64* scratch, cudaStream_t st);
+// Hoisted rotations of ONE source ct into R outputs (one per step).
+void rotate_hoisted(const Dev& d, int R, int l, const u64* src, const u32* gal,
+                    const u64* const* keys, ItemPtr out, u64* scratch, cudaStream_t st);
+
+// ---- rescale (optionally fused with a plaintext-mask multiply after it)
+size_t rescale_scratch_elems(int B, int npoly, u32 n);
+void rescale_batch(const Dev& d, int B, int l, int npoly, ItemPtr in, ItemPtr out,
+                   ItemPtr mask_mont, u64* scratch, cudaStream_t st);
+
+// ---- elementwise
+void tensor_batch(const Dev& d, int B, int l, ItemPtr a, ItemPtr b, ItemPtr out, cudaStream_t st);
+void mult_pt_batch(const Dev& d, int B, int l, int npoly, ItemPtr ct, ItemPtr pt, ItemPtr out,
+                   bool pt_mont, cudaStream_t st);
+void add_batch(const Dev& d, int B, int l, int npoly, ItemPtr a, ItemPtr b, ItemPtr out,
+               cudaStream_t st);
+// acc[poly][m] += sum_b src(b)[poly][m]   (mod q_m), nl limbs per poly
+void accumulate(const Dev& d, int B, int nl, int npoly, ItemPtr src, u64* acc, cudaStream_t st);
+void to_montgomery(const Dev& d, u64* buf, size_t nlimb_total, const PrimeMap& pm, bool inverse,
+                   cudaStream_t st);
+// limbs[l][j] = coeffs[j] mod q_{pm[l]} for signed int64 coefficients
+void signed_to_limbs(const Dev& d, const long long* coeffs, int nl, const PrimeMap& pm, u64* out,
+                     cudaStream_t st);
+// KSK assembly: b[i][m] = ntt_e[i][m] + [m<=L] f[i][m] target[m] - a[i][m] sk[m]
+void ksk_combine(const Dev& d, u64* key, const u64* ntt_e, const u64* target, const u64* sk,
+                 const ulonglong2* f, cudaStream_t st);
+// Encryption combine: c0 = v pk_b + e0 + pt ; c1 = v pk_a + e1 (all NTT form, nl limbs)
+void encrypt_combine(const Dev& d, int nl, const u64* v, const u64* pkb, const u64* pka,
+                     const u64* e0, const u64* e1, const u64* pt, u64* ct, cudaStream_t st);
+// Decrypt: pt[i] = c0[i] + c1[i] s[i]
+void decrypt_combine(const Dev& d, int nl, const u64* ct, const u64* sk, u64* pt, cudaStream_t st);
+
+// data[i] mod q for limbs after an integer-sum collective
+void reduce_mod(const Dev& d, u64* data, int npoly, int nl, cudaStream_t st);
+
+// Seam kernels (single prime given by value, nlimb limbs of n)
+enum SeamOp { SEAM_ADD, SEAM_SUB, SEAM_NEG, SEAM_MUL, SEAM_SCALAR, SEAM_FMA, SEAM_EXTEND };
+void seam_op(int op, size_t count, const u64* a, const u64* b, u64* out, PrimeConst P, u64 s,
+             u64 q_src, cudaStream_t st);
+
+}  // namespace hs

@@ -1,0 +1,388 @@
+// The encrypted SpMSpM runner: CSR x CSC planner + batched device executor.
+//
+// Replaces the reference's timed region `spmm_csr_csc` -> `_run_schedule`
+// -> `fhe_spmspm_step` (engine.py:99-184; encmat.py:150-221).  The reference
+// walks pairs one at a time; here the pair list is planned on the host and
+// executed in phases, each a handful of batched kernel launches:
+//
+//   1. alignment  distinct (operand, step) rotations only, hoisted: one
+//                 decompose+ModUp per source operand, then per step the
+//                 automorphism-gathered key inner product + ModDown.
+//   2. pairs      per batch of B pairs: mult_ct fused into relinearisation
+//                 (tensor computed on the fly in the digit loader and the
+//                 ModDown epilogue), rescale fused with the mask multiply,
+//                 second rescale, accumulation rotation (pairs sorted by
+//                 step so equal keys are adjacent), modular accumulation.
+//
+// Bit-exactness of this re-ordering: each pair's
+// contribution is computed exactly as the reference computes it, and the
+// final modular sum is order-free.
+#include <algorithm>
+#include <chrono>
+#include <numeric>
+#include <unordered_map>
+
+#include "../../include/hespmm_b200.h"
+#include "ops.cuh"
+
+using namespace hs;
+typedef unsigned __int128 u128;
+
+namespace {
+
+struct PlanPair {
+    int64_t i, j, ap, bp;
+};
+
+u32 norm_step(int64_t s, u32 slots) {
+    int64_t r = s % (int64_t)slots;
+    if (r < 0) r += slots;
+    return (u32)r;
+}
+
+u64 powmod_h(u64 b, u64 e, u64 q) {
+    u64 r = 1 % q;
+    b %= q;
+    while (e) {
+        if (e & 1) r = (u64)((u128)r * b % q);
+        b = (u64)((u128)b * b % q);
+        e >>= 1;
+    }
+    return r;
+}
+
+// Two-pointer intersection per output cell (encmat.py:170-186).
+template <class Emit>
+void merge_pairs(int dim, const int64_t* oa, const int64_t* ia, const int64_t* ob, const int64_t* ib,
+                 Emit emit) {
+    for (int i = 0; i < dim; i++) {
+        const int64_t a0 = oa[i], a1 = oa[i + 1];
+        if (a0 == a1) continue;
+        for (int j = 0; j < dim; j++) {
+            int64_t x = a0, y = ob[j];
+            const int64_t y1 = ob[j + 1];
+            while (x < a1 && y < y1) {
+                const int64_t c = ia[x], r = ib[y];
+                if (c == r) {
+                    emit(PlanPair{i, j, x, y});
+                    x++;
+                    y++;
+                } else if (c < r) {
+                    x++;
+                } else {
+                    y++;
+                }
+            }
+        }
+    }
+}
+
+struct DeviceArena {
+    cudaStream_t st;
+    std::vector<void*> ptrs;
+    bool failed = false;
+    template <class T>
+    T* get(size_t count) {
+        void* p = nullptr;
+        if (count == 0) count = 1;
+        if (cudaMallocAsync(&p, count * sizeof(T), st) != cudaSuccess) {
+            failed = true;
+            return nullptr;
+        }
+        ptrs.push_back(p);
+        return (T*)p;
+    }
+    ~DeviceArena() {
+        for (void* p : ptrs) cudaFreeAsync(p, st);
+    }
+};
+
+hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, const u64* ct_a,
+                    const u64* ct_b, const u64* const* masks, int64_t nmasks, u64* out,
+                    hs_counters* cnt, int shard, int nshard, cudaStream_t st,
+                    std::chrono::steady_clock::time_point t_start) {
+    const int L = c->L;
+    const u32 n = c->n, slots = n / 2;
+    const Dev& d = c->dev;
+    hs_counters C{};
+    if (L < 2) {
+        set_error("insufficient depth: need at least 2 levels");
+        return (hs_status)HS_EVAL_ERROR;
+    }
+    if (nshard < 1 || shard < 0 || shard >= nshard) {
+        set_error("bad shard index/count");
+        return (hs_status)HS_PARAMETER_ERROR;
+    }
+    const int64_t np = (int64_t)pairs.size();
+
+    // ---- plan: per pair sources, mask, accumulation key (logical counts over all pairs)
+    std::vector<int32_t> ia(np), ib(np);
+    std::vector<u32> accr(np);
+    std::vector<int64_t> mpos(np);
+    std::unordered_map<u64, int32_t> align_idx;      // key = src * slots + r
+    std::vector<std::pair<int, u32>> align_list;     // (src, r)
+    auto galois_key = [&](int64_t raw, u32 r) -> const u64* {
+        auto it = c->galois.find(r);
+        if (it == c->galois.end()) {
+            set_error("missing Galois key for step " + std::to_string(raw));
+            return nullptr;
+        }
+        return it->second.d;
+    };
+    if (!c->relin.d && np) {
+        set_error("no relinearization key in bundle");
+        return (hs_status)HS_KEY_MISSING;
+    }
+    for (int64_t p = 0; p < np; p++) {
+        const PlanPair& q = pairs[p];
+        int64_t mn;
+        ia[p] = 0;
+        ib[p] = 1;
+        if (q.ap != q.bp) {
+            const int src = q.ap < q.bp ? 1 : 0;          // the higher-positioned operand rotates
+            const int64_t raw = q.ap < q.bp ? q.bp - q.ap : q.ap - q.bp;
+            const u32 r = norm_step(raw, slots);
+            C.rotations++;
+            C.alignment_rotations++;
+            if (r) {
+                if (!galois_key(raw, r)) return (hs_status)HS_KEY_MISSING;
+                const u64 key = (u64)src * slots + r;
+                auto it = align_idx.find(key);
+                int32_t idx;
+                if (it == align_idx.end()) {
+                    idx = 2 + (int32_t)align_list.size();
+                    align_idx.emplace(key, idx);
+                    align_list.push_back({src, r});
+                } else {
+                    idx = it->second;
+                }
+                (src ? ib[p] : ia[p]) = idx;
+            }
+            mn = std::min(q.ap, q.bp);
+        } else {
+            mn = q.ap;
+        }
+        const int64_t rot = mn - (q.i * dim + q.j);
+        accr[p] = 0;
+        if (rot != 0) {
+            C.rotations++;
+            C.accumulation_rotations++;
+            const u32 r = norm_step(rot, slots);
+            if (r && !galois_key(rot, r)) return (hs_status)HS_KEY_MISSING;
+            accr[p] = r;
+        }
+        if (mn < 0 || mn >= nmasks || !masks[mn]) {
+            set_error("mask for slot " + std::to_string(mn) + " not prewarmed");
+            return (hs_status)HS_EVAL_ERROR;
+        }
+        mpos[p] = mn;
+    }
+    C.ct_ct_mults = C.pt_mults = C.relins = C.relin_noops = np;
+    C.rescales = 2 * np;
+    C.adds = np > 0 ? np - 1 : 0;
+    C.has_result = np > 0;
+
+    // ---- shard: pairs sorted by accumulation step, contiguous ranges
+    std::vector<int64_t> order(np);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int64_t x, int64_t y) { return accr[x] < accr[y]; });
+    const int64_t lo = np * shard / nshard, hi = np * (shard + 1) / nshard;
+    const int64_t P = hi - lo;
+    C.pairs = P;
+
+    // alignments this shard needs, compacted
+    std::vector<int32_t> slot_of(2 + align_list.size(), -1);
+    std::vector<int32_t> need;
+    for (int64_t t = lo; t < hi; t++) {
+        for (int32_t idx : {ia[order[t]], ib[order[t]]})
+            if (idx >= 2 && slot_of[idx] < 0) {
+                slot_of[idx] = (int32_t)need.size();
+                need.push_back(idx);
+            }
+    }
+    C.physical_alignment = (int64_t)need.size();
+    const auto t_plan = std::chrono::steady_clock::now();
+    C.plan_ms = std::chrono::duration<double, std::milli>(t_plan - t_start).count();
+
+    const size_t ctL = (size_t)2 * (L + 1) * n;           // ct at level L
+    const size_t ctL2 = (size_t)2 * (L - 1) * n;          // ct at level L-2
+    HS_CUDA(cudaMemsetAsync(out, 0, ctL2 * sizeof(u64), st));
+    if (P == 0) {
+        *cnt = C;
+        return (hs_status)HS_OK;
+    }
+
+    DeviceArena A{st};
+    const size_t budget = c->batch_bytes;
+
+    // ---- phase 1: hoisted alignment rotations
+    u64* aligned = A.get<u64>(need.size() * ctL);
+    if (A.failed) {
+        set_error("out of device memory for aligned operands");
+        return (hs_status)HS_OUT_OF_MEMORY;
+    }
+    for (int src = 0; src < 2; src++) {
+        std::vector<u32> gal;
+        std::vector<const u64*> keys;
+        std::vector<const u64*> outs;
+        for (size_t k = 0; k < need.size(); k++) {
+            const auto& al = align_list[need[k] - 2];
+            if (al.first != src) continue;
+            gal.push_back((u32)powmod_h(5, al.second, 2ull * n));
+            keys.push_back(c->galois[al.second].d);
+            outs.push_back(aligned + k * ctL);
+        }
+        const int R = (int)gal.size();
+        if (!R) continue;
+        const size_t base_e = ks_hoisted_scratch_elems(0, L, n);
+        const size_t per_e = ks_hoisted_scratch_elems(1, L, n) - base_e;
+        int64_t rmax = budget / 8 > base_e ? (int64_t)((budget / 8 - base_e) / per_e) : 1;
+        rmax = std::max<int64_t>(1, std::min<int64_t>(rmax, R));
+        u64* scratch = A.get<u64>(ks_hoisted_scratch_elems((int)rmax, L, n));
+        u32* d_gal = A.get<u32>(R);
+        const u64** d_keys = A.get<const u64*>(R);
+        const u64** d_outs = A.get<const u64*>(R);
+        if (A.failed) {
+            set_error("out of device memory (alignment)");
+            return (hs_status)HS_OUT_OF_MEMORY;
+        }
+        HS_CUDA(cudaMemcpyAsync(d_gal, gal.data(), R * sizeof(u32), cudaMemcpyHostToDevice, st));
+        HS_CUDA(cudaMemcpyAsync(d_keys, keys.data(), R * sizeof(u64*), cudaMemcpyHostToDevice, st));
+        HS_CUDA(cudaMemcpyAsync(d_outs, outs.data(), R * sizeof(u64*), cudaMemcpyHostToDevice, st));
+        const u64* sp = src ? ct_b : ct_a;
+        for (int r0 = 0; r0 < R; r0 += (int)rmax) {
+            const int rc = std::min<int>((int)rmax, R - r0);
+            rotate_hoisted(d, rc, L, sp, d_gal + r0, d_keys + r0, table(d_outs + r0), scratch, st);
+        }
+    }
+
+    // ---- phase 2: pair batches
+    std::vector<const u64*> hA(P), hB(P), hM(P), hK(P);
+    std::vector<u32> hG(P);
+    for (int64_t t = 0; t < P; t++) {
+        const int64_t p = order[lo + t];
+        hA[t] = ia[p] >= 2 ? aligned + (size_t)slot_of[ia[p]] * ctL : ct_a;
+        hB[t] = ib[p] >= 2 ? aligned + (size_t)slot_of[ib[p]] * ctL : ct_b;
+        hM[t] = masks[mpos[p]];
+        hK[t] = accr[p] ? c->galois[accr[p]].d : nullptr;
+        hG[t] = accr[p] ? (u32)powmod_h(5, accr[p], 2ull * n) : 0u;
+    }
+    const size_t per_pair = ks_scratch_elems(1, L, n) +
+                            (size_t)n * (2 * (L + 1) + 2 * L + 4 * (L - 1) + 2);
+    int64_t B = std::max<int64_t>(1, std::min<int64_t>((int64_t)(budget / 8 / per_pair), P));
+    B = std::min<int64_t>(B, 8192);
+    const u64** dA = A.get<const u64*>(P);
+    const u64** dB = A.get<const u64*>(P);
+    const u64** dM = A.get<const u64*>(P);
+    const u64** dK = A.get<const u64*>(P);
+    const u64** dR = A.get<const u64*>(B);
+    u32* dG = A.get<u32>(P);
+    u64* ks = A.get<u64>(ks_scratch_elems((int)B, L, n));
+    u64* Rb = A.get<u64>((size_t)B * 2 * (L + 1) * n);
+    u64* Mb = A.get<u64>((size_t)B * 2 * L * n);
+    u64* Cb = A.get<u64>((size_t)B * ctL2);
+    u64* Fb = A.get<u64>((size_t)B * ctL2);
+    u64* Tb = A.get<u64>((size_t)B * 2 * n);
+    if (A.failed) {
+        set_error("out of device memory (pair batch)");
+        return (hs_status)HS_OUT_OF_MEMORY;
+    }
+    std::vector<const u64*> relin_rep(B, c->relin.d);
+    HS_CUDA(cudaMemcpyAsync(dA, hA.data(), P * sizeof(u64*), cudaMemcpyHostToDevice, st));
+    HS_CUDA(cudaMemcpyAsync(dB, hB.data(), P * sizeof(u64*), cudaMemcpyHostToDevice, st));
+    HS_CUDA(cudaMemcpyAsync(dM, hM.data(), P * sizeof(u64*), cudaMemcpyHostToDevice, st));
+    HS_CUDA(cudaMemcpyAsync(dK, hK.data(), P * sizeof(u64*), cudaMemcpyHostToDevice, st));
+    HS_CUDA(cudaMemcpyAsync(dG, hG.data(), P * sizeof(u32), cudaMemcpyHostToDevice, st));
+    HS_CUDA(cudaMemcpyAsync(dR, relin_rep.data(), B * sizeof(u64*), cudaMemcpyHostToDevice, st));
+
+    for (int64_t s = 0; s < P; s += B) {
+        const int bn = (int)std::min<int64_t>(B, P - s);
+        int z = 0;
+        while (z < bn && hG[s + z] == 0) z++;
+        // mult_ct + relinearize (fused), level L
+        mult_relin_batch(d, bn, L, table(dA + s), table(dB + s), dR, strided(Rb, (size_t)2 * (L + 1) * n),
+                         ks, st);
+        // rescale L -> L-1 fused with the mask product (mask in Montgomery form)
+        rescale_batch(d, bn, L, 2, strided(Rb, (size_t)2 * (L + 1) * n), strided(Mb, (size_t)2 * L * n),
+                      table(dM + s), Tb, st);
+        // relinearize of a degree-1 ct is a counted no-op (context.py:368-370)
+        // rescale L-1 -> L-2
+        rescale_batch(d, bn, L - 1, 2, strided(Mb, (size_t)2 * L * n), strided(Cb, ctL2),
+                      ItemPtr{nullptr, nullptr, 0}, Tb, st);
+        // accumulation rotations (step-0 pairs form the sorted prefix)
+        if (bn - z > 0)
+            rotate_batch(d, bn - z, L - 2, strided(Cb + (size_t)z * ctL2, ctL2), dG + s + z, dK + s + z,
+                         strided(Fb + (size_t)z * ctL2, ctL2), ks, st);
+        accumulate(d, z, L - 1, 2, strided(Cb, ctL2), out, st);
+        accumulate(d, bn - z, L - 1, 2, strided(Fb + (size_t)z * ctL2, ctL2), out, st);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error(std::string("kernel launch failed: ") + cudaGetErrorString(e));
+        return (hs_status)HS_CUDA_ERROR;
+    }
+    *cnt = C;
+    return (hs_status)HS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+hs_status hs_plan_csr_csc(int32_t dim, const int64_t* oa, const int64_t* ia, const int64_t* ob,
+                          const int64_t* ib, int64_t* pairs, int64_t cap, int64_t* npairs) {
+    int64_t cntp = 0;
+    merge_pairs(dim, oa, ia, ob, ib, [&](const PlanPair& p) {
+        if (cntp < cap) {
+            pairs[4 * cntp] = p.i;
+            pairs[4 * cntp + 1] = p.j;
+            pairs[4 * cntp + 2] = p.ap;
+            pairs[4 * cntp + 3] = p.bp;
+        }
+        cntp++;
+    });
+    *npairs = cntp;
+    return (hs_status)HS_OK;
+}
+
+hs_status hs_spmspm_csr_csc(hs_ctx* c, int32_t dim, const int64_t* oa, const int64_t* ia,
+                            const int64_t* ob, const int64_t* ib, const uint64_t* ct_a,
+                            const uint64_t* ct_b, const uint64_t* const* masks, int64_t nmasks,
+                            uint64_t* out, hs_counters* counters, int32_t shard, int32_t nshard,
+                            void* stream) {
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<PlanPair> pairs;
+    merge_pairs(dim, oa, ia, ob, ib, [&](const PlanPair& p) { pairs.push_back(p); });
+    return run_pairs(c, dim, pairs, ct_a, ct_b, masks, nmasks, out, counters, shard, nshard,
+                     (cudaStream_t)stream, t0);
+}
+
+hs_status hs_spmspm_pairs(hs_ctx* c, int32_t dim, const int64_t* pl, int64_t np, const uint64_t* ct_a,
+                          const uint64_t* ct_b, const uint64_t* const* masks, int64_t nmasks,
+                          uint64_t* out, hs_counters* counters, int32_t shard, int32_t nshard,
+                          void* stream) {
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<PlanPair> pairs(np);
+    for (int64_t p = 0; p < np; p++) pairs[p] = PlanPair{pl[4 * p], pl[4 * p + 1], pl[4 * p + 2], pl[4 * p + 3]};
+    return run_pairs(c, dim, pairs, ct_a, ct_b, masks, nmasks, out, counters, shard, nshard,
+                     (cudaStream_t)stream, t0);
+}
+
+hs_status hs_reduce_mod(hs_ctx* c, uint64_t* data, int32_t npoly, int32_t nlimbs, void* stream) {
+    if (nlimbs < 1 || nlimbs > c->L + 1) {
+        set_error("bad limb count");
+        return (hs_status)HS_PARAMETER_ERROR;
+    }
+    reduce_mod(c->dev, data, npoly, nlimbs, (cudaStream_t)stream);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error(std::string("kernel launch failed: ") + cudaGetErrorString(e));
+        return (hs_status)HS_CUDA_ERROR;
+    }
+    return (hs_status)HS_OK;
+}
+
+void hs_set_batch_bytes(hs_ctx* c, uint64_t bytes) { c->batch_bytes = bytes; }
+
+}  // extern "C"

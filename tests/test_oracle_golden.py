@@ -1,0 +1,161 @@
+"""Pin the CPU oracle against golden vectors produced by the real reference.
+
+tests/golden/make_golden.py ran the reference package (Cython backend) in the
+build container; these tests re-create the same inputs from the recorded
+seeds and require the oracle to reproduce every digest bit for bit.
+"""
+
+import numpy as np
+import pytest
+
+from helpers import digest, kernel_inputs, parse_key
+
+
+def test_chains_match_reference(golden, oracle_mod):
+    O = oracle_mod
+    for key, rec in golden["chains"].items():
+        n, sb, L, seed = parse_key(key)
+        P = O.build_params(n, sb, L, seed)
+        assert list(P.modulus_chain) == rec["chain"], key
+        assert P.aux_prime == rec["aux"], key
+
+
+def test_product_chain_restatement_matches_reference(golden):
+    from paper_2604_11659_b200.params import build_params
+    for key, rec in golden["chains"].items():
+        n, sb, L, seed = parse_key(key)
+        P = build_params(n, sb, L, seed)
+        assert list(P.modulus_chain) == rec["chain"], key
+        assert P.aux_prime == rec["aux"], key
+
+
+@pytest.mark.parametrize("key", ["64_35_2_3", "1024_45_2_2024", "16384_50_2_2024",
+                                 "65536_50_2_2024"])
+def test_limb_kernels_match_reference(golden, oracle_mod, key):
+    O = oracle_mod
+    n, sb, L, seed = parse_key(key)
+    P = O.build_params(n, sb, L, seed)
+    ctx = O.OracleContext(P)
+    for pi_s, rec in golden["kernels"][key].items():
+        pi = int(pi_s)
+        q = rec["q"]
+        t = ctx.tables(pi)
+        assert t["mu"] == rec["mu"] and t["n_inv"] == rec["n_inv"]
+        dg = rec["digests"]
+        for name in ("roots", "roots_sh", "iroots", "iroots_sh"):
+            assert digest(t[name]) == dg[name], (key, pi, name)
+        a, b, acc, s = kernel_inputs(q, n, pi)
+        outs = {
+            "ntt": O.ntt(a, q, t["roots"], t["roots_sh"]),
+            "intt": O.intt(a, q, t["iroots"], t["iroots_sh"], t["n_inv"]),
+            "add": O.add_mod(a, b, q), "sub": O.sub_mod(a, b, q), "neg": O.neg_mod(a, q),
+            "mul": O.mul_mod(a, b, q, t["mu"]), "scalar": O.scalar_mul_mod(a, s, q),
+            "extend": O.extend_mod(a, q, rec["q_dst"]),
+        }
+        f = acc.copy()
+        O.fma_mod(f, a, b, q, t["mu"])
+        outs["fma"] = f
+        for name, v in outs.items():
+            assert digest(v) == dg[name], (key, pi, name)
+
+
+def _ops_pipeline(O, key):
+    """Re-create make_golden.py section 3 with the oracle."""
+    n, sb, L, seed = parse_key(key)
+    P = O.build_params(n, sb, L, seed)
+    ctx = O.OracleContext(P)
+    keys = ctx.keygen()
+    slots = P.slots
+    rng = np.random.default_rng(77)
+    va = rng.uniform(-1, 1, min(slots, 16))
+    vb = rng.uniform(-1, 1, min(slots, 16))
+    ct_a = ctx.encrypt(ctx.encode(va), keys)
+    ct_b = ctx.encrypt(ctx.encode(vb), keys)
+    ctx.gen_galois_keys([1, 3, slots - 1, -2, 5], keys)
+    return P, ctx, keys, ct_a, ct_b
+
+
+@pytest.mark.parametrize("key", ["64_40_2_7", "64_40_3_7", "1024_45_2_2024", "16384_50_2_2024"])
+def test_ckks_primitives_match_reference(golden, oracle_mod, key):
+    O = oracle_mod
+    rec = golden["ops"][key]
+    P, ctx, keys, (ca, sa, la), (cb, sbb, lb) = _ops_pipeline(O, key)
+    L = P.levels
+    slots = P.slots
+    dg = rec["digests"]
+    assert digest(keys.secret.astype(np.uint64) & np.uint64(0xFF)) == rec["secret"]
+    assert digest(keys.pk_b) == rec["pk_b"] and digest(keys.pk_a) == rec["pk_a"]
+    assert digest(keys.relin[0]) == rec["relin_b"] and digest(keys.relin[1]) == rec["relin_a"]
+    for r, (hb, ha) in rec["galois"].items():
+        assert digest(keys.galois[int(r)][0]) == hb and digest(keys.galois[int(r)][1]) == ha
+    assert digest(ca) == dg["ct_a"] and digest(cb) == dg["ct_b"]
+    assert sa == rec["scale_a"] and sbb == rec["scale_b"]
+    m3 = ctx.eval_mult_ct(ca, cb, L)
+    assert digest(m3) == dg["mult_ct"]
+    r1 = ctx.relinearize(m3, keys.relin, L)
+    assert digest(r1) == dg["relin"]
+    s1 = ctx.rescale(r1, L)
+    assert digest(s1) == dg["rescale"]
+    mask, mscale, _ = ctx.encode(np.eye(1, min(slots, 16), 2).ravel(), scale=float(P.modulus_chain[L - 1]),
+                                 level=L - 1)
+    assert digest(mask) == dg["mask"]
+    mp = ctx.eval_mult_pt(s1, mask, L - 1)
+    assert digest(mp) == dg["mult_pt"]
+    s2 = ctx.rescale(mp, L - 1)
+    assert digest(s2) == dg["rescale2"]
+    assert digest(ctx.eval_add(ca, cb, L)) == dg["add"]
+    for r in (1, 3, slots - 1, slots - 2, 5):
+        assert digest(ctx.eval_rotate(ca, r, keys.galois, L)) == dg[f"rot_L_{r}"], r
+        assert digest(ctx.eval_rotate(s2, r, keys.galois, L - 2)) == dg[f"rot_low_{r}"], r
+    # float scale ledger
+    sc = rec["scales"]
+    s = sa * sbb
+    assert s == sc["mult_ct"]
+    s = s / P.modulus_chain[L]
+    assert s == sc["rescale"]
+    s = s * mscale
+    assert s == sc["mult_pt"]
+    assert s / P.modulus_chain[L - 1] == sc["rescale2"]
+    dec = ctx.decode(ctx.decrypt(s2, keys, L - 2), sc["rescale2"])
+    assert [float(x) for x in dec[:16]] == rec["decoded_rescale2_first16"]
+
+
+def oracle_runner_case(O, n, sb, L, seed, dim, sparsity, mseed):
+    P = O.build_params(n, sb, L, seed)
+    ctx = O.OracleContext(P)
+    keys = ctx.keygen()
+    a = O.generate_random_sparse(dim, sparsity, (mseed, 0))
+    b = O.generate_random_sparse(dim, sparsity, (mseed, 1))
+    oa, ia, va = O.csr_pack(a)
+    ob, ib, vb = O.csc_pack(b)
+    ca = ctx.encrypt(ctx.encode(va), keys)
+    cb = ctx.encrypt(ctx.encode(vb), keys)
+    pairs = O.pair_schedule_csr_csc(oa, ia, ob, ib, dim)
+    steps = O.rotation_steps(pairs, dim)
+    ctx.gen_galois_keys(steps, keys)
+    pos = sorted({min(p[2], p[3]) for p in pairs})
+    masks = {p: ctx.encode(np.eye(1, dim * dim, p).ravel(), scale=float(P.modulus_chain[L - 1]),
+                           level=L - 1)[0] for p in pos}
+    res = ctx.spmspm(ca[0], cb[0], pairs, dim, masks, keys)
+    return P, ctx, keys, a, b, ca, cb, pairs, res
+
+
+def test_runner_matches_reference(golden, oracle_mod):
+    O = oracle_mod
+    for key, rec in golden["runner"].items():
+        n, sb, L, seed = rec["params"]
+        P, ctx, keys, a, b, ca, cb, pairs, res = oracle_runner_case(
+            O, n, sb, L, seed, rec["dim"], rec["sparsity"], rec["mseed"])
+        assert digest(ca[0]) == rec["ct_a"] and digest(cb[0]) == rec["ct_b"], key
+        assert len(pairs) == rec["counters"]["ct_ct_mults"], key
+        if rec["result"] is None:
+            assert res is None
+            continue
+        assert digest(res) == rec["result"], key
+        scale = ((ca[1] * cb[1]) / P.modulus_chain[L] * float(P.modulus_chain[L - 1])) \
+            / P.modulus_chain[L - 1]
+        assert scale == rec["scale"]
+        dec = ctx.decode(ctx.decrypt(res, keys, L - 2), scale)[: rec["dim"] ** 2]
+        out = dec.reshape(rec["dim"], rec["dim"])
+        assert repr(O.frobenius_error(out, O.plain_matmul(a, b))) == rec["frobenius"], key
+        assert digest(out.view(np.uint64)) == rec["decoded"], key
