@@ -1,0 +1,396 @@
+#!/usr/bin/env python
+"""Benchmark: encrypted SpMSpM (CKKS, CSR/C) on B200 -- BASELINE.json metric.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+A "step" is one full encrypted SpMSpM (the reference's timed region:
+planning + every pair, engine.py:176-184) of the workload below.  Inputs
+(the two encrypted matrices, keys, masks) are resident in HBM for ``value``;
+``e2e`` repeats the step through the public API with host-resident
+ciphertexts (host->device copy of both operands and device->host copy of the
+result inside the timed region).
+
+Workload (BASELINE.json configs[1], the largest single-GPU config whose keys
+fit one B200): ring degree 2^14, Delta = 2^50, L = 2, 64x64 @ 75% sparsity,
+matrices from the reference harness seeds (bench.py:93-96 of the reference:
+cell seed 1*1_000_003 + 64*1_009), params seed 2024.
+
+Metric: ct-ops/s = logical OpCounter total (ct_ct_mults + pt_mults +
+rotations + relins + rescales + adds; relin no-ops excluded) / seconds, and
+ms per matmul.  Multi-GPU (torchrun, one rank per GPU): pairs are sharded
+(strong scaling: fixed matmul), partial results combined by one NCCL SUM.
+
+``--impl reference`` times the reference algorithm on the host CPU instead:
+the CPU oracle (oracle/, a C restatement of the reference path, bit-exact,
+OpenMP over pairs) on a bounded sample of the same workload's pairs.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "cfg2": dict(ring_degree=1 << 14, scale_bits=50, levels=2, seed=2024, dim=64, sparsity=0.75,
+                 desc="configs[1]: N=2^14, 64x64 @75% sparsity, single B200"),
+    "cfg1": dict(ring_degree=1 << 10, scale_bits=45, levels=2, seed=2024, dim=16, sparsity=0.5,
+                 desc="configs[0]: desk-small params (pkg/params), 16x16 @50%"),
+}
+
+
+def cell_seed(dim: int) -> int:
+    return 1 * 1_000_003 + dim * 1_009 + 0
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ----------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# -------------------------------------------------------------- workload
+
+def make_inputs(pkg, wl):
+    from paper_2604_11659_b200 import encmat, engine, formats
+    params = pkg.build_params(wl["ring_degree"], wl["scale_bits"], wl["levels"], wl["seed"])
+    t0 = time.time()
+    ctx = pkg.CkksContext(params)
+    keys = ctx.keygen()
+    seed = cell_seed(wl["dim"])
+    a = formats.generate_random_sparse(wl["dim"], wl["sparsity"], (seed, 0))
+    b = formats.generate_random_sparse(wl["dim"], wl["sparsity"], (seed, 1))
+    ea = encmat.encrypt_sparse(a, encmat.Layout.CSR, ctx, keys)
+    eb = encmat.encrypt_sparse(b, encmat.Layout.CSC, ctx, keys)
+    steps = encmat.required_rotation_steps(ea.meta, eb.meta)
+    keys = ctx.gen_galois_keys(steps, keys)
+    pairs = encmat.pair_array(ea.meta, eb.meta)
+    mc = engine.MaskCache(ctx, wl["dim"])
+    mc.prewarm(np.unique(np.minimum(pairs[:, 2], pairs[:, 3])))
+    import torch
+    torch.cuda.synchronize()
+    log(f"[bench] setup {time.time() - t0:.1f}s: {len(pairs)} pairs, {len(steps)} rotation steps, "
+        f"{len(keys.galois)} Galois keys")
+    return params, ctx, keys, a, b, ea, eb, pairs, mc
+
+
+def logical_ct_ops(pairs: np.ndarray, dim: int) -> int:
+    """OpCounter total of the reference for a pair list (engine.py:99-160)."""
+    p = len(pairs)
+    if p == 0:
+        return 0
+    align = int(np.count_nonzero(pairs[:, 2] != pairs[:, 3]))
+    accum = int(np.count_nonzero(np.minimum(pairs[:, 2], pairs[:, 3]) != pairs[:, 0] * dim + pairs[:, 1]))
+    return p + p + (align + accum) + p + 2 * p + (p - 1)   # ct_ct, pt, rot, relin, rescale, add
+
+
+# ------------------------------------------------------------ CPU baseline
+
+def cpu_oracle_sample(wl, sample_pairs: int, nthreads: int):
+    """Time the CPU oracle (reference algorithm restated in C, bit-exact) on
+    the first ``sample_pairs`` pairs of the workload.  Returns (seconds,
+    ct_ops, pairs_used).  Keys for the sampled steps only."""
+    from oracle import oracle as O
+    P = O.build_params(wl["ring_degree"], wl["scale_bits"], wl["levels"], wl["seed"])
+    ctx = O.OracleContext(P)
+    keys = ctx.keygen()
+    dim = wl["dim"]
+    seed = cell_seed(dim)
+    a = O.generate_random_sparse(dim, wl["sparsity"], (seed, 0))
+    b = O.generate_random_sparse(dim, wl["sparsity"], (seed, 1))
+    oa, ia, va = O.csr_pack(a)
+    ob, ib, vb = O.csc_pack(b)
+    ca = ctx.encrypt(ctx.encode(va), keys)
+    cb = ctx.encrypt(ctx.encode(vb), keys)
+    pairs = O.pair_schedule_csr_csc(oa, ia, ob, ib, dim)[:sample_pairs]
+    ctx.gen_galois_keys(O.rotation_steps(pairs, dim), keys)
+    L = P.levels
+    masks = {p: ctx.encode(np.eye(1, dim * dim, p).ravel(), scale=float(P.modulus_chain[L - 1]),
+                           level=L - 1)[0] for p in {min(x[2], x[3]) for x in pairs}}
+    t0 = time.perf_counter()
+    ctx.spmspm(ca[0], cb[0], pairs, dim, masks, keys, nthreads=nthreads)
+    dt = time.perf_counter() - t0
+    return dt, logical_ct_ops(np.array(pairs, dtype=np.int64).reshape(-1, 4), dim), len(pairs)
+
+
+# ------------------------------------------------------------- roofline
+
+def roofline_probe(pkg, ctx, params, peaks):
+    """Time the dominant kernel alone with CUDA events on its launch stream.
+
+    Dominant kernel: the NTT pass kernel (ntt_pass_kernel), which carries
+    decomposition, ModUp, ModDown and rescale (see profiles/).  Probe: one
+    batched forward NTT over the ModUp limb count of a pair batch; one launch
+    = one pass over every limb; algorithmic bytes per launch = limbs * 16 n
+    (each limb read once, written once).
+    """
+    import torch
+    from paper_2604_11659_b200 import device as D
+    from paper_2604_11659_b200._lib import check, lib
+    n, L = params.ring_degree, params.levels
+    items = 512
+    limbs = items * (L + 1) * (L + 2)
+    buf = D.zeros((limbs, n))
+    st = torch.cuda.current_stream()
+    for _ in range(3):
+        check(lib().hs_ntt(ctx.handle, D.ptr(buf), items * (L + 1), L + 2, 0, 0, D.stream()))
+    reps = 10
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(reps):
+        check(lib().hs_ntt(ctx.handle, D.ptr(buf), items * (L + 1), L + 2, 0, 0, D.stream()))
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / (reps * 2)           # two pass launches per NTT
+    algo = limbs * 16 * n
+    achieved = algo / (ms * 1e-3) / 1e9
+    peak = peaks.get("hbm_gbs", 6650.0)
+    butterflies = limbs * (n // 2) * (n.bit_length() - 1) / 2      # per pass
+    return {"kernel": "ntt_pass_kernel (batched 2-pass NTT, one pass)", "bound": "hbm",
+            "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": None,
+            "launch_ms": round(ms, 4), "algorithmic_bytes_per_launch": algo,
+            "butterflies_per_launch": int(butterflies),
+            "peak_source": "MEASURED_PEAKS.json" if "hbm_gbs" in peaks else "fallback"}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except OSError:
+        return {}
+
+
+# ------------------------------------------------------------------ arms
+
+def run_reference_arm(args, wl):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    nthreads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        pass                                    # the CPU oracle has no warm-up state
+    times, ops = [], 0
+    for _ in range(args.steps):
+        dt, ops, used = cpu_oracle_sample(wl, args.cpu_sample_pairs, nthreads)
+        times.append(dt)
+    sec = float(np.mean(times))
+    value = ops / sec
+    line = {
+        "impl": "reference", "metric": "encrypted SpMSpM ct-ops/s (CSR/C)", "value": value,
+        "unit": "ct-ops/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": wl["desc"], "ring_degree": wl["ring_degree"],
+                   "levels": wl["levels"], "scale_bits": wl["scale_bits"], "dim": wl["dim"],
+                   "sparsity": wl["sparsity"], "sample_pairs": used},
+        "cpu_baseline": {"value": value, "unit": "ct-ops/s", "cores": nthreads, "kind": "port",
+                         "sample": f"first {used} pairs of the CSR/C schedule per step "
+                                   "(oracle/hs_oracle.c, OpenMP over pairs)"},
+        "e2e": {"value": value, "unit": "ct-ops/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_b200_arm(args, wl):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2604_11659_b200 as pkg
+    from paper_2604_11659_b200 import device as D
+    from paper_2604_11659_b200 import dist as hdist
+    from paper_2604_11659_b200 import encmat, engine
+    from paper_2604_11659_b200._lib import lib
+    from paper_2604_11659_b200.types import Ciphertext
+
+    params, ctx, keys, a, b, ea, eb, pairs, mc = make_inputs(pkg, wl)
+    dim = wl["dim"]
+    ct_ops = logical_ct_ops(pairs, dim)
+
+    def step(ea_, eb_):
+        c = engine.OpCounter()
+        if world > 1:
+            return hdist.spmm_csr_csc_distributed(ea_, eb_, ctx, keys, c, mc), c
+        return engine.spmm_csr_csc(ea_, eb_, ctx, keys, c, mc), c
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+    res, c = step(ea, eb)
+    assert c.ct_ops() == ct_ops
+    for _ in range(max(0, args.warmup - 1)):
+        step(ea, eb)
+    torch.cuda.synchronize()
+
+    # ---- device-resident timed region
+    st = torch.cuda.current_stream()
+    launches0 = lib().hs_launch_count()
+    total_ms = 0.0
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            res, c = step(ea, eb)
+            e1.record(st)
+            torch.cuda.synchronize()
+            total_ms += e0.elapsed_time(e1)
+    launches = lib().hs_launch_count() - launches0
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms = total_ms / args.steps
+    value = ct_ops / (ms * 1e-3)
+
+    # ---- end to end through the public API from pinned host buffers
+    host_a = torch.from_numpy(ea.ctxt.host()).pin_memory()
+    host_b = torch.from_numpy(eb.ctxt.host()).pin_memory()
+    e2e_s = 0.0
+    d2h = 0
+    for _ in range(args.steps):
+        flush.fill_(1)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ha = encmat.EncryptedSparseMatrix(Ciphertext(host_a, ea.ctxt.scale, ea.ctxt.level), ea.meta)
+        hb = encmat.EncryptedSparseMatrix(Ciphertext(host_b, eb.ctxt.scale, eb.ctxt.level), eb.meta)
+        r, _ = step(ha, hb)
+        out = r.ctxt.host()
+        e2e_s += time.perf_counter() - t0
+        d2h = out.nbytes
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = ct_ops / (e2e_s / args.steps)
+
+    # ---- bit-exactness spot check of the timed result (cheap: vs the first run)
+    same = bool(np.array_equal(res.ctxt.host(), out))
+
+    peaks = load_peaks()
+    roof = roofline_probe(pkg, ctx, params, peaks) if rank == 0 else None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        nthreads = os.cpu_count() or 1
+        dt, ops_s, used = cpu_oracle_sample(wl, args.cpu_sample_pairs, nthreads)
+        cpu = {"value": ops_s / dt, "unit": "ct-ops/s", "cores": nthreads, "kind": "port",
+               "sample": f"first {used} of {len(pairs)} pairs (oracle/hs_oracle.c, OpenMP), "
+                         f"{dt:.1f}s"}
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        line = {
+            "metric": "encrypted SpMSpM ct-ops/s (CSR/C)", "value": value, "unit": "ct-ops/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "ms_per_matmul": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": wl["desc"], "ring_degree": wl["ring_degree"],
+                       "levels": wl["levels"], "scale_bits": wl["scale_bits"], "dim": wl["dim"],
+                       "sparsity": wl["sparsity"], "pairs": int(len(pairs)), "ct_ops": ct_ops,
+                       "galois_keys": len(keys.galois), "parallelism": f"pair-shard x{world}",
+                       "l2": "flushed between steps (256 MiB write)"},
+            "e2e": {"value": e2e_value, "unit": "ct-ops/s",
+                    "h2d_bytes_per_step": int(host_a.numel() * 8 + host_b.numel() * 8),
+                    "d2h_bytes_per_step": int(d2h), "ms_per_matmul": e2e_s / args.steps * 1e3},
+            "gpu_launches": int(launches),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "result_repeatable": same,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--cpu-sample-pairs", type=int, default=256)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference_arm(args, wl)
+    else:
+        run_b200_arm(args, wl)
+
+
+if __name__ == "__main__":
+    main()

@@ -129,6 +129,16 @@ hs_status hs_ctx_create(hs_ctx** out, int device, uint32_t n, uint32_t levels,
         return (hs_status)HS_PARAMETER_ERROR;
     }
     HS_CUDA(cudaSetDevice(device));
+    {
+        // The runner's per-call work buffers come from the stream-ordered pool;
+        // keep freed blocks cached instead of returning them to the driver at
+        // every synchronisation (re-mapping GBs per matmul costs 100s of ms).
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t thr = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
     hs_ctx* c = new hs_ctx();
     c->device = device;
     c->n = n;
@@ -436,8 +446,6 @@ struct SeamTables {
     PrimeConst* pc = nullptr;
     ulonglong2* tw = nullptr;
 };
-std::mutex g_seam_mu;
-std::map<std::tuple<u64, u32, const u64*, const u64*, int>, SeamTables> g_seam;
 }  // namespace
 
 extern "C" {
@@ -448,28 +456,18 @@ hs_status hs_seam_ntt(uint64_t* a, uint32_t n, uint64_t q, const uint64_t* roots
         set_error("bad ring degree");
         return (hs_status)HS_PARAMETER_ERROR;
     }
-    int dev = 0;
-    cudaGetDevice(&dev);
+    // Tables are rebuilt per call from the caller's arrays (the seam is for API
+    // compatibility, not the hot path), so no stale cache can alias them.
+    cudaStream_t st = ST(stream);
+    PrimeConst P = make_prime_const(q, n);
+    P.n_inv = n_inv;
+    P.n_inv_sh = (u64)(((u128)n_inv << 64) / q);
     SeamTables t;
-    {
-        std::lock_guard<std::mutex> lk(g_seam_mu);
-        auto key = std::make_tuple((u64)q, (u32)n, (const u64*)roots, (const u64*)roots_sh, dev);
-        auto it = g_seam.find(key);
-        if (it == g_seam.end()) {
-            PrimeConst P = make_prime_const(q, n);
-            P.n_inv = n_inv;
-            P.n_inv_sh = (u64)(((u128)n_inv << 64) / q);
-            HS_CUDA(cudaMalloc(&t.pc, sizeof(PrimeConst)));
-            HS_CUDA(cudaMalloc(&t.tw, (size_t)n * sizeof(ulonglong2)));
-            HS_CUDA(cudaMemcpy(t.pc, &P, sizeof(P), cudaMemcpyHostToDevice));
-            zip_kernel<<<(n + 255) / 256, 256>>>(roots, roots_sh, t.tw, n);
-            note_launch();
-            HS_CUDA(cudaDeviceSynchronize());
-            g_seam[key] = t;
-        } else {
-            t = it->second;
-        }
-    }
+    HS_CUDA(cudaMallocAsync((void**)&t.pc, sizeof(PrimeConst), st));
+    HS_CUDA(cudaMallocAsync((void**)&t.tw, (size_t)n * sizeof(ulonglong2), st));
+    HS_CUDA(cudaMemcpyAsync(t.pc, &P, sizeof(P), cudaMemcpyHostToDevice, st));
+    zip_kernel<<<(n + 255) / 256, 256, 0, st>>>(roots, roots_sh, t.tw, n);
+    note_launch();
     Dev d{};
     d.n = n;
     d.log_n = __builtin_ctz(n);
@@ -478,8 +476,11 @@ hs_status hs_seam_ntt(uint64_t* a, uint32_t n, uint64_t q, const uint64_t* roots
     d.tw = t.tw;
     d.itw = t.tw;
     PrimeMap pm = prime_map_range(0, 1);
-    ntt_plain(d, a, nullptr, 1, pm, !inverse, ST(stream));
+    ntt_plain(d, a, nullptr, 1, pm, !inverse, st);
     CHECK_LAUNCH();
+    HS_CUDA(cudaStreamSynchronize(st));   // P lives on this stack frame
+    cudaFreeAsync(t.pc, st);
+    cudaFreeAsync(t.tw, st);
     return (hs_status)HS_OK;
 }
 

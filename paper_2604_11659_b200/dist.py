@@ -36,8 +36,8 @@ def reduce_partials(partial: torch.Tensor, moduli, group=None) -> torch.Tensor:
 def host_mod(summed: np.ndarray, moduli) -> np.ndarray:
     """Reference reduction used by the CPU (gloo) tests."""
     out = summed.astype(np.uint64).copy()
-    for m, q in enumerate(moduli):
-        out[:, m] %= np.uint64(q)
+    for m in range(out.shape[1]):
+        out[:, m] %= np.uint64(moduli[m])
     return out
 
 
