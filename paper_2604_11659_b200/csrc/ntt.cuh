@@ -27,16 +27,107 @@
 
 namespace hs {
 
-constexpr int NTT_TILE = 2048;      // elements per CTA tile (16 KiB smem)
-constexpr int NTT_THREADS = 256;    // 4 butterflies per thread per stage
+constexpr int NTT_TILE = 2048;      // elements per CTA tile (16 KiB smem + padding)
+constexpr int NTT_EPT = 8;          // elements per thread (radix-8 register rounds)
+constexpr int NTT_THREADS = NTT_TILE / NTT_EPT;
+
+// Shared-memory index with one pad word per 8 (keeps the stride-8 accesses of
+// the lowest-bit round at the 2-wavefront minimum).
+HS_DEV u32 spad(u32 i) { return i + (i >> 3); }
+
+// One register round: local stages [A, A+R) of a tile with H rows, G = 2^LOGG
+// group elements and C columns.  A "unit" is the 2^R elements that differ in
+// the round's bits; each thread owns 8 / 2^R units, 8 elements in registers.
+template <bool FWD, int LOGG, int H, int C, int A, int R>
+__device__ __forceinline__ void ntt_round(u64* sm, const ulonglong2* __restrict__ tw, u32 hi0,
+                                          int s0, u64 q, u64 two_q) {
+    constexpr int G = 1 << LOGG;
+    constexpr int TILE = H * G * C;
+    constexpr int T = TILE / NTT_EPT;
+    constexpr int NU = 1 << R;
+    constexpr int UPT = NTT_EPT / NU;
+    constexpr int LOWB = LOGG - A - R;
+#pragma unroll
+    for (int k = 0; k < UPT; k++) {
+        const u32 U = threadIdx.x + k * T;
+        const u32 c = U % C;
+        const u32 rest = U / C;
+        const u32 go = rest % (G >> R);
+        const u32 h = rest / (G >> R);
+        const u32 go_high = go >> LOWB;
+        const u32 go_low = go & ((1u << LOWB) - 1);
+        const u32 gbase = (go_high << (LOWB + R)) | go_low;
+        const u32 hi = hi0 + h;
+        u64 v[NU];
+#pragma unroll
+        for (int e = 0; e < NU; e++) v[e] = sm[spad((h * G + (gbase | ((u32)e << LOWB))) * C + c)];
+        if (FWD) {
+#pragma unroll
+            for (int j = 0; j < R; j++) {
+                const int ls = A + j;
+                const u32 base = (1u << (s0 + ls)) + (hi << ls) + (go_high << j);
+                constexpr int dummy = 0;
+                (void)dummy;
+#pragma unroll
+                for (int e = 0; e < NU; e++) {
+                    const int bit = 1 << (R - 1 - j);
+                    if (e & bit) continue;
+                    const ulonglong2 w = tw[base + (e >> (R - j))];
+                    u64 x = csub(v[e], two_q);
+                    const u64 t = shoup_lazy(v[e + bit], w.x, w.y, q);
+                    v[e] = x + t;
+                    v[e + bit] = x - t + two_q;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int j = R - 1; j >= 0; j--) {
+                const int ls = A + j;
+                const u32 base = (1u << (s0 + ls)) + (hi << ls) + (go_high << j);
+#pragma unroll
+                for (int e = 0; e < NU; e++) {
+                    const int bit = 1 << (R - 1 - j);
+                    if (e & bit) continue;
+                    const ulonglong2 w = tw[base + (e >> (R - j))];
+                    const u64 x = v[e], y = v[e + bit];
+                    v[e] = csub(x + y, two_q);
+                    v[e + bit] = shoup_lazy(x - y + two_q, w.x, w.y, q);
+                }
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < NU; e++) sm[spad((h * G + (gbase | ((u32)e << LOWB))) * C + c)] = v[e];
+    }
+}
+
+template <int LOGG, int H, int C, int A>
+__device__ __forceinline__ void ntt_rounds_fwd(u64* sm, const ulonglong2* tw, u32 hi0, int s0,
+                                               u64 q, u64 two_q) {
+    if constexpr (A < LOGG) {
+        constexpr int R = (LOGG - A) < 3 ? (LOGG - A) : 3;
+        ntt_round<true, LOGG, H, C, A, R>(sm, tw, hi0, s0, q, two_q);
+        __syncthreads();
+        ntt_rounds_fwd<LOGG, H, C, A + R>(sm, tw, hi0, s0, q, two_q);
+    }
+}
+
+template <int LOGG, int H, int C, int TOP>
+__device__ __forceinline__ void ntt_rounds_inv(u64* sm, const ulonglong2* tw, u32 hi0, int s0,
+                                               u64 q, u64 two_q) {
+    if constexpr (TOP > 0) {
+        constexpr int R = TOP < 3 ? TOP : 3;
+        ntt_round<false, LOGG, H, C, TOP - R, R>(sm, tw, hi0, s0, q, two_q);
+        __syncthreads();
+        ntt_rounds_inv<LOGG, H, C, TOP - R>(sm, tw, hi0, s0, q, two_q);
+    }
+}
 
 template <bool FWD, bool FIRST, bool LAST, int LOGG, int H, int C, class Job>
 __global__ void __launch_bounds__(NTT_THREADS)
 ntt_pass_kernel(Dev d, Job job, int s0, int jbase) {
     constexpr int G = 1 << LOGG;
     constexpr int TILE = H * G * C;
-    constexpr int NB = TILE / 2;     // butterflies per stage
-    __shared__ u64 sm[TILE];
+    __shared__ u64 sm[TILE + TILE / 8];
 
     const int log_n = d.log_n;
     const int s1 = s0 + LOGG;
@@ -44,7 +135,6 @@ ntt_pass_kernel(Dev d, Job job, int s0, int jbase) {
     const int jb = jbase + (int)blockIdx.y;
     const int p = job.prime(jb);
     const PrimeConst P = d.pc[p];
-    const u64 q = P.q, two_q = P.two_q;
     const ulonglong2* __restrict__ tw = (FWD ? d.tw : d.itw) + (size_t)p * d.n;
 
     const u32 ncolblk = (1u << lo_bits) / C;
@@ -57,48 +147,20 @@ ntt_pass_kernel(Dev d, Job job, int s0, int jbase) {
     };
 
     if (FIRST) {
-        for (u32 e = threadIdx.x; e < TILE; e += blockDim.x) sm[e] = job.load(jb, gidx(e), P);
+        for (u32 e = threadIdx.x; e < TILE; e += blockDim.x) sm[spad(e)] = job.load(jb, gidx(e), P);
     } else {
         const u64* __restrict__ src = job.scratch(jb);
-        for (u32 e = threadIdx.x; e < TILE; e += blockDim.x) sm[e] = src[gidx(e)];
+        for (u32 e = threadIdx.x; e < TILE; e += blockDim.x) sm[spad(e)] = src[gidx(e)];
     }
     __syncthreads();
-
-#pragma unroll 1
-    for (int st = 0; st < LOGG; st++) {
-        const int ls = FWD ? st : LOGG - 1 - st;     // local stage
-        const int s = s0 + ls;                        // global stage
-        const u32 lhalf = LOGG - 1 - ls;              // log2(half)
-        const u32 half = 1u << lhalf;
-        for (u32 u = threadIdx.x; u < NB; u += blockDim.x) {
-            const u32 c = u % C;
-            const u32 rest = u / C;
-            const u32 b = rest % (G / 2);
-            const u32 h = rest / (G / 2);
-            const u32 blk = b >> lhalf, off = b & (half - 1);
-            const u32 g0 = (blk << (lhalf + 1)) + off;
-            const u32 i0 = (h * G + g0) * C + c;
-            const u32 i1 = i0 + half * C;
-            const ulonglong2 w = tw[(1u << s) + ((hi0 + h) << ls) + blk];
-            u64 x = sm[i0], y = sm[i1];
-            if (FWD) {
-                x = csub(x, two_q);
-                const u64 t = shoup_lazy(y, w.x, w.y, q);
-                sm[i0] = x + t;
-                sm[i1] = x - t + two_q;
-            } else {
-                sm[i0] = csub(x + y, two_q);
-                sm[i1] = shoup_lazy(x - y + two_q, w.x, w.y, q);
-            }
-        }
-        __syncthreads();
-    }
+    if (FWD) ntt_rounds_fwd<LOGG, H, C, 0>(sm, tw, hi0, s0, P.q, P.two_q);
+    else ntt_rounds_inv<LOGG, H, C, LOGG>(sm, tw, hi0, s0, P.q, P.two_q);
 
     if (LAST) {
-        for (u32 e = threadIdx.x; e < TILE; e += blockDim.x) job.store(jb, gidx(e), sm[e], P);
+        for (u32 e = threadIdx.x; e < TILE; e += blockDim.x) job.store(jb, gidx(e), sm[spad(e)], P);
     } else {
         u64* __restrict__ dst = job.scratch(jb);
-        for (u32 e = threadIdx.x; e < TILE; e += blockDim.x) dst[gidx(e)] = sm[e];
+        for (u32 e = threadIdx.x; e < TILE; e += blockDim.x) dst[gidx(e)] = sm[spad(e)];
     }
 }
 
@@ -106,8 +168,7 @@ ntt_pass_kernel(Dev d, Job job, int s0, int jbase) {
 template <bool FWD, int LOGN, class Job>
 void launch_ntt_single(const Dev& d, const Job& job, int jbase, int njobs, cudaStream_t st) {
     dim3 grid(1, njobs);
-    int threads = (1 << LOGN) / 2 < NTT_THREADS ? (1 << LOGN) / 2 : NTT_THREADS;
-    if (threads < 1) threads = 1;
+    const int threads = (1 << LOGN) / NTT_EPT;
     ntt_pass_kernel<FWD, true, true, LOGN, 1, 1, Job><<<grid, threads, 0, st>>>(d, job, 0, jbase);
     note_launch();
 }
@@ -122,7 +183,7 @@ void launch_ntt_two(const Dev& d, const Job& job, int jbase, int njobs, cudaStre
     const u32 n = 1u << (LA + LB);
     dim3 grid(n / NTT_TILE, njobs);
     note_launch(2);
-    if (FWD) {
+    if constexpr (FWD) {
         ntt_pass_kernel<true, true, false, LA, 1, CA, Job><<<grid, NTT_THREADS, 0, st>>>(d, job, 0, jbase);
         ntt_pass_kernel<true, false, true, LB, HB, 1, Job><<<grid, NTT_THREADS, 0, st>>>(d, job, LA, jbase);
     } else {

@@ -13,6 +13,7 @@
 #include "ops.cuh"
 
 #include <atomic>
+#include <cstdlib>
 
 namespace hs {
 
@@ -302,6 +303,106 @@ static void mod_down(const Dev& d, int B, int l, const u64* ACC, u64* T, const A
     launch_ntt<true>(d, JobModDown<Add>{T, ACC, out, add, l, d}, B * 2 * (l + 1), st);
 }
 
+// Fused ModUp second pass + key inner product.  One CTA owns a contiguous
+// 2048-element tile of target modulus m for item b; for every digit i it
+// finishes the NTT of lift(digit_i) on that tile in shared memory (the first
+// pass already ran, writing lazy values into E[b][i][m]) and folds the tile
+// into 128-bit accumulators against the key tile; the ModUp output is never
+// written back to HBM.  Digit i == m contributes x_i * df_i (already in E).
+template <int LA, int LB, int MINB>
+__global__ void __launch_bounds__(NTT_THREADS, MINB)
+modup_inner_kernel(Dev d, int l, const u64* __restrict__ E, const u64* const* __restrict__ keys,
+                   u64* __restrict__ ACC) {
+    constexpr int H = NTT_TILE >> LB;
+    __shared__ u64 sm[NTT_TILE + NTT_TILE / 8];
+    const u32 n = d.n;
+    const int m = blockIdx.y, b = blockIdx.z;
+    const int pm = m <= l ? m : d.L + 1;
+    const PrimeConst P = d.pc[pm];
+    const ulonglong2* __restrict__ tw = d.tw + (size_t)pm * n;
+    const u32 hi0 = blockIdx.x * H;
+    const u32 j0 = hi0 << LB;
+    const u32 t = threadIdx.x;
+    const size_t kst = (size_t)(d.L + 2) * n;
+    const u64* __restrict__ key = keys[b];
+    const u64* kb = key + (size_t)pm * n + j0;
+    const u64* ka = key + (size_t)(d.L + 1) * kst + (size_t)pm * n + j0;
+    const u64* Eb = E + (size_t)b * (l + 1) * (l + 2) * n;
+    u64 lb[NTT_EPT], hb[NTT_EPT], la[NTT_EPT], ha[NTT_EPT];
+#pragma unroll
+    for (int k = 0; k < NTT_EPT; k++) lb[k] = hb[k] = la[k] = ha[k] = 0;
+    for (int i = 0; i <= l; i++) {
+        const u64* src = Eb + ((size_t)i * (l + 2) + m) * n + j0;
+        u64 ext[NTT_EPT];
+        if (i == m) {
+#pragma unroll
+            for (int k = 0; k < NTT_EPT; k++) ext[k] = src[t + k * NTT_THREADS];
+        } else {
+#pragma unroll
+            for (int k = 0; k < NTT_EPT; k++) sm[spad(t + k * NTT_THREADS)] = src[t + k * NTT_THREADS];
+            __syncthreads();
+            ntt_rounds_fwd<LB, H, 1, 0>(sm, tw, hi0, LA, P.q, P.two_q);
+#pragma unroll
+            for (int k = 0; k < NTT_EPT; k++) ext[k] = canon4(sm[spad(t + k * NTT_THREADS)], P);
+            __syncthreads();
+        }
+        const u64* kbi = kb + (size_t)i * kst;
+        const u64* kai = ka + (size_t)i * kst;
+#pragma unroll
+        for (int k = 0; k < NTT_EPT; k++) {
+            mac128(lb[k], hb[k], ext[k], kbi[t + k * NTT_THREADS]);
+            mac128(la[k], ha[k], ext[k], kai[t + k * NTT_THREADS]);
+        }
+    }
+    u64* out = ACC + (size_t)b * 2 * (l + 2) * n + j0;
+#pragma unroll
+    for (int k = 0; k < NTT_EPT; k++) {
+        out[(size_t)m * n + t + k * NTT_THREADS] = redc128(lb[k], hb[k], P);
+        out[(size_t)(l + 2 + m) * n + t + k * NTT_THREADS] = redc128(la[k], ha[k], P);
+    }
+}
+
+template <int LA, int LB>
+static void launch_modup_inner(const Dev& d, int B, int l, u64* D, u64* E, const u64* const* keys,
+                               u64* ACC, cudaStream_t st) {
+    const u32 n = d.n;
+    JobModUp job{D, E, l, d.L, n, d.pc};
+    constexpr int CA = NTT_TILE >> LA;
+    const int njobs = B * (l + 1) * (l + 1);
+    for (int base = 0; base < njobs; base += 65535) {
+        const int cnt = njobs - base < 65535 ? njobs - base : 65535;
+        ntt_pass_kernel<true, true, false, LA, 1, CA, JobModUp>
+            <<<dim3(n / NTT_TILE, cnt), NTT_THREADS, 0, st>>>(d, job, 0, base);
+        note_launch();
+    }
+    // HS_MODUP_MINB=1 trades occupancy for registers (A/B knob for profiling)
+    static const int minb = getenv("HS_MODUP_MINB") ? atoi(getenv("HS_MODUP_MINB")) : 2;
+    if (minb == 1)
+        modup_inner_kernel<LA, LB, 1><<<dim3(n / NTT_TILE, l + 2, B), NTT_THREADS, 0, st>>>(d, l, E, keys, ACC);
+    else
+        modup_inner_kernel<LA, LB, 2><<<dim3(n / NTT_TILE, l + 2, B), NTT_THREADS, 0, st>>>(d, l, E, keys, ACC);
+    note_launch();
+}
+
+// ModUp + inner product for B items (E must hold x_i df_i in slot (i, i)).
+static void modup_and_inner(const Dev& d, int B, int l, u64* D, u64* E, const u64* const* keys,
+                            u64* ACC, cudaStream_t st) {
+    switch (d.log_n) {
+        case 12: launch_modup_inner<6, 6>(d, B, l, D, E, keys, ACC, st); return;
+        case 13: launch_modup_inner<6, 7>(d, B, l, D, E, keys, ACC, st); return;
+        case 14: launch_modup_inner<7, 7>(d, B, l, D, E, keys, ACC, st); return;
+        case 15: launch_modup_inner<7, 8>(d, B, l, D, E, keys, ACC, st); return;
+        case 16: launch_modup_inner<8, 8>(d, B, l, D, E, keys, ACC, st); return;
+        case 17: launch_modup_inner<8, 9>(d, B, l, D, E, keys, ACC, st); return;
+        default: break;
+    }
+    // small rings: whole-limb single-pass NTT, then the plain inner product
+    launch_ntt<true>(d, JobModUp{D, E, l, d.L, d.n, d.pc}, B * (l + 1) * (l + 1), st);
+    dim3 g((d.n + 255) / 256, l + 2, B);
+    ks_inner_kernel<<<g, 256, 0, st>>>(d, l, E, (size_t)(l + 1) * (l + 2) * d.n, keys, nullptr, ACC);
+    note_launch();
+}
+
 template <class Src, class Add>
 static void key_switch_batch(const Dev& d, int B, int l, const Src& src, const Add& add,
                              const u64* const* keys, ItemPtr out, u64* scratch, cudaStream_t st) {
@@ -311,10 +412,7 @@ static void key_switch_batch(const Dev& d, int B, int l, const Src& src, const A
     u64* ACC = D + (size_t)B * (l + 1) * n;
     u64* T = ACC + (size_t)B * 2 * (l + 2) * n;
     launch_ntt<false>(d, JobDecompose<Src>{src, E, D, d.df, l, n, d}, B * (l + 1), st);
-    launch_ntt<true>(d, JobModUp{D, E, l, d.L, n, d.pc}, B * (l + 1) * (l + 1), st);
-    dim3 g((n + 255) / 256, l + 2, B);
-    ks_inner_kernel<<<g, 256, 0, st>>>(d, l, E, (size_t)(l + 1) * (l + 2) * n, keys, nullptr, ACC);
-    note_launch();
+    modup_and_inner(d, B, l, D, E, keys, ACC, st);
     mod_down(d, B, l, ACC, T, add, out, st);
 }
 
