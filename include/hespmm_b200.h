@@ -84,6 +84,26 @@ hs_status hs_key_upload(hs_ctx* ctx, int kind, uint32_t step, const uint64_t* ke
 hs_status hs_key_generate(hs_ctx* ctx, int kind, uint32_t step, const uint64_t* a,
                           const int64_t* e, const uint64_t* target, const uint64_t* sk,
                           void* stream);
+/* ---- on-device Galois key generation (keygen.cu), bit-exact with
+ * gen_galois_keys (context.py:176-200): each key's numpy stream
+ * default_rng(SeedSequence((seed, 0x90, r))) is replayed on the GPU
+ * (PCG64 XSL-RR, Lemire bounded uint64, ziggurat normal). */
+/* numpy's ziggurat tables as compiled into the installed numpy (host pointers). */
+hs_status hs_keygen_set_tables(hs_ctx* ctx, const double* wi, const double* fi, const uint64_t* ki);
+/* Secret key in NTT form over all L+2 primes (device pointer, copied). */
+hs_status hs_keygen_set_secret(hs_ctx* ctx, const uint64_t* sk_ntt, void* stream);
+/* pcg_states: per step {state_hi, state_lo, inc_hi, inc_lo} of the numpy PCG64
+ * *before* its first draw (host array).  generate_galois: make the keys now
+ * into the key store; register: make them on demand inside the runner (keys
+ * that do not fit in HBM, e.g. 8.8 TB at N=2^16, L=24). */
+hs_status hs_key_generate_galois(hs_ctx* ctx, const uint32_t* steps, const uint64_t* pcg_states,
+                                 int32_t nsteps, void* stream);
+hs_status hs_keygen_register(hs_ctx* ctx, const uint32_t* steps, const uint64_t* pcg_states,
+                             int32_t nsteps);
+/* Raw draws only (testing): a [K][L+1][L+2][n] uniform limbs, e [K][L+1][n] int64 (device). */
+hs_status hs_keygen_streams(hs_ctx* ctx, const uint64_t* pcg_states, int32_t nkeys, uint64_t* a_out,
+                            int64_t* e_out, void* stream);
+int64_t hs_keys_generated(const hs_ctx* ctx);
 /* Standard-form copy [2][L+1][L+2][n] into device buffer `out`. */
 hs_status hs_key_download(hs_ctx* ctx, int kind, uint32_t step, uint64_t* out, void* stream);
 int hs_key_has(const hs_ctx* ctx, int kind, uint32_t step);

@@ -44,6 +44,15 @@ _SIGS = {
     "hs_key_generate": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_uint32, c_vp, c_vp, c_vp, c_vp,
                                        c_vp]),
     "hs_key_download": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_uint32, c_vp, c_vp]),
+    "hs_keygen_set_tables": (ctypes.c_int, [c_vp, ctypes.POINTER(ctypes.c_double),
+                                            ctypes.POINTER(ctypes.c_double), c_u64p]),
+    "hs_keygen_set_secret": (ctypes.c_int, [c_vp, c_vp, c_vp]),
+    "hs_key_generate_galois": (ctypes.c_int, [c_vp, ctypes.POINTER(ctypes.c_uint32), c_u64p,
+                                              ctypes.c_int32, c_vp]),
+    "hs_keygen_register": (ctypes.c_int, [c_vp, ctypes.POINTER(ctypes.c_uint32), c_u64p,
+                                          ctypes.c_int32]),
+    "hs_keygen_streams": (ctypes.c_int, [c_vp, c_u64p, ctypes.c_int32, c_vp, c_vp, c_vp]),
+    "hs_keys_generated": (ctypes.c_int64, [c_vp]),
     "hs_key_has": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_uint32]),
     "hs_key_drop": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_uint32]),
     "hs_key_count": (ctypes.c_int64, [c_vp]),

@@ -103,8 +103,19 @@ class CkksContext:
     def _download_key(self, kind: int, step: int) -> np.ndarray:
         L, n = self._L, self._n
         out = D.empty((2, L + 1, L + 2, n))
+        lazy = kind == 1 and step in getattr(self, "_lazy_steps", ()) and \
+            not lib().hs_key_has(self._h, 1, step)
+        if lazy:        # materialise a lazily registered key just for the copy
+            from .rng import galois_states
+            st = np.ascontiguousarray(galois_states(self.params.seed, [step]))
+            check(lib().hs_key_generate_galois(self._h, (ctypes.c_uint32 * 1)(step),
+                                               st.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                                               1, D.stream()))
         check(lib().hs_key_download(self._h, kind, step, D.ptr(out), D.stream()))
-        return D.to_host(out)
+        host = D.to_host(out)
+        if lazy:
+            check(lib().hs_key_drop(self._h, 1, step))
+        return host
 
     def upload_key(self, kind: int, step: int, key: np.ndarray) -> KeySwitchKey:
         """Install a standard-form key [2][L+1][L+2][n] (e.g. made elsewhere)."""
@@ -183,19 +194,54 @@ class CkksContext:
         neg[t[~lo] - n] = True
         return src, neg
 
-    def gen_galois_keys(self, steps, keys: KeyBundle) -> KeyBundle:
+    def _ensure_device_keygen(self, keys: KeyBundle) -> None:
+        if getattr(self, "_keygen_secret", None) is keys.secret:
+            return
+        from .rng import ziggurat_tables
+        wi, fi, ki = ziggurat_tables()
+        check(lib().hs_keygen_set_tables(
+            self._h, wi.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+            fi.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+            ki.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))))
+        check(lib().hs_keygen_set_secret(self._h, D.ptr(self._sk_ntt(keys)), D.stream()))
+        self._keygen_secret = keys.secret
+
+    def gen_galois_keys(self, steps, keys: KeyBundle, device=False) -> KeyBundle:
         """Rotation keys for ``steps``; per-step seeded, so order-independent
-        (context.py:176-200)."""
+        (context.py:176-200).
+
+        ``device=False`` draws the numpy stream on the host (the reference's
+        own calls) and assembles on the GPU; ``device=True`` replays each
+        step's stream on the GPU (csrc/keygen.cu, bit-identical keys);
+        ``device="lazy"`` only registers the steps -- the runner generates
+        each key on the GPU when it needs it and frees it afterwards (keys
+        that do not fit in HBM, e.g. 8.8 TB at N=2^16, L=24).
+        """
         slots = self.params.slots
         extra = {}
-        sk = self._sk_ntt(keys)
-        secret = keys.secret.astype(np.int64)
+        todo = []
         for step in steps:
             if step == 0 or abs(step) >= slots:
                 raise ParameterError(f"rotation step {step} out of range")
             r = step % slots
-            if r in keys.galois or r in extra:
+            if r in keys.galois or r in extra or r in todo:
                 continue
+            todo.append(r)
+        if device and todo:
+            from .rng import galois_states
+            self._ensure_device_keygen(keys)
+            st = np.ascontiguousarray(galois_states(self.params.seed, todo))
+            arr = (ctypes.c_uint32 * len(todo))(*todo)
+            stp = st.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))
+            if device == "lazy":
+                check(lib().hs_keygen_register(self._h, arr, stp, len(todo)))
+                self._lazy_steps = getattr(self, "_lazy_steps", set()) | set(todo)
+            else:
+                check(lib().hs_key_generate_galois(self._h, arr, stp, len(todo), D.stream()))
+            return keys.with_galois({r: KeySwitchKey(self, 1, r) for r in todo})
+        sk = self._sk_ntt(keys)
+        secret = keys.secret.astype(np.int64)
+        for r in todo:
             rng = np.random.default_rng(np.random.SeedSequence(entropy=(self.params.seed, 0x90, r)))
             src, neg = self._perm_tables(pow(5, r, 2 * self._n))
             rotated = secret[src] * np.where(neg, -1, 1)

@@ -247,6 +247,8 @@ void hs_ctx_destroy(hs_ctx* c) {
     cudaDeviceSynchronize();
     if (c->relin.d) cudaFree(c->relin.d);
     for (auto& kv : c->galois) cudaFree(kv.second.d);
+    for (void* p : {(void*)c->d_jump, (void*)c->d_zig, (void*)c->d_thr, (void*)c->d_sk, (void*)c->d_kskf})
+        if (p) cudaFree(p);
     if (c->d_blob) cudaFree(c->d_blob);
     delete c;
 }

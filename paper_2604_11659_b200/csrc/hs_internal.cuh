@@ -48,6 +48,16 @@ struct hs_ctx {
     std::vector<u64> df, auxinv;             // host copies (plain values)
     std::vector<u64> qlinv;                  // [(L+1)*(L+1)]
     void* d_blob = nullptr;                  // one allocation for all tables
+    // on-device Galois key generation (keygen.cu)
+    void* d_jump = nullptr;                  // PCG64 LCG jump constants
+    void* d_zig = nullptr;                   // numpy ziggurat tables
+    u64* d_thr = nullptr;                    // Lemire thresholds per prime
+    u64* d_sk = nullptr;                     // secret key, NTT form [L+2][n]
+    ulonglong2* d_kskf = nullptr;            // p (Q_L/q_i) mod q_m, Shoup pairs [(L+1)^2]
+    struct Stream { u64 s_hi, s_lo, i_hi, i_lo; };
+    std::unordered_map<u32, Stream> lazy;    // registered steps generated on demand
+    size_t keygen_batch = 16;                // keys generated per launch
+    int64_t keys_generated = 0;
     hs::KeyBuf relin;
     size_t batch_bytes = (size_t)6 << 30;   // runner work-buffer budget
     std::unordered_map<u32, hs::KeyBuf> galois;   // normalised step -> key
@@ -64,3 +74,10 @@ struct hs_ctx {
                                                    : HS_CUDA_ERROR;            \
         }                                                                      \
     } while (0)
+
+namespace hs {
+// Generate Galois keys on the device into `dests` ([2][L+1][L+2][n] each).
+hs_status generate_galois_keys(hs_ctx* c, const std::vector<u32>& steps,
+                               const std::vector<hs_ctx::Stream>& streams,
+                               const std::vector<u64*>& dests, cudaStream_t st);
+}  // namespace hs

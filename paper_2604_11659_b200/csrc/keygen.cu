@@ -1,0 +1,616 @@
+// On-device Galois key generation, bit-exact with the reference's
+// gen_galois_keys (ckks/context.py:176-200 -> _make_ksk :150-174).
+//
+// The reference draws every key from its own numpy stream
+//   rng = default_rng(SeedSequence(entropy=(seed, 0x90, r)))     (PCG64)
+// in this order, per digit i = 0..L:
+//   (L+2) x rng.integers(0, q_m, n, uint64)   -- Lemire bounded ints, 64-bit
+//   rng.normal(0, 3.2, n) -> rint -> int64     -- ziggurat (256 layers)
+// and assembles b[i][m] = NTT(e_i mod q_m) + [m<=L] p(Q_L/q_i) sk(X^g) - a[i][m] sk.
+//
+// Here one CTA replays one key's stream in order, 1024 positions per chunk:
+// every thread advances its own PCG64 state by 1024 per chunk (precomputed
+// LCG jump constants), raw outputs go to a two-chunk shared-memory ring, and
+// the block consumes them segment by segment:
+//   uniform: accept iff low64(x*q) >= (2^64 - q) mod q (Lemire's rejection
+//            rule), value = high64(x*q); block scan assigns output indices;
+//   normal:  ziggurat fast path in parallel (rabs < ki[idx]); the token parse
+//            (slow tokens consume 2 draws, tail tokens 1+2k) is walked by one
+//            thread over a fast-path bitmap; block scan assigns indices.
+// The SeedSequence -> PCG64 state and the ziggurat tables (read from the
+// installed numpy binary and validated against numpy on the host) are inputs.
+#include <algorithm>
+#include <cstring>
+
+#include "ops.cuh"
+
+namespace hs {
+
+constexpr int RNG_T = 1024;             // threads per key CTA = positions per chunk
+
+struct U128 {
+    u64 hi, lo;
+};
+
+HS_DEV U128 mul128(U128 a, U128 b) {    // mod 2^128
+    U128 r;
+    r.lo = a.lo * b.lo;
+    r.hi = __umul64hi(a.lo, b.lo) + a.lo * b.hi + a.hi * b.lo;
+    return r;
+}
+HS_DEV U128 add128(U128 a, U128 b) {
+    U128 r;
+    r.lo = a.lo + b.lo;
+    r.hi = a.hi + b.hi + (r.lo < a.lo ? 1ull : 0ull);
+    return r;
+}
+HS_DEV u64 xsl_rr(U128 s) {
+    const u64 x = s.hi ^ s.lo;
+    const unsigned rot = (unsigned)(s.hi >> 58);
+    return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+
+struct ZigTables {
+    double wi[256];
+    double fi[256];
+    u64 ki[256];
+};
+
+struct RngJump {                          // for t = 0..RNG_T: A_t = M^t, S_t = sum_{k<t} M^k
+    U128 A[RNG_T + 1];
+    U128 S[RNG_T + 1];
+};
+
+struct KeyStream {
+    u64 state_hi, state_lo, inc_hi, inc_lo;   // numpy PCG64 state before the first draw
+};
+
+struct KeygenArgs {
+    const KeyStream* streams;              // [K]
+    u64* const* a_out;                     // [K] -> [L+1][L+2][n] (a half of the key)
+    long long* e_out;                      // [K][L+1][n]
+    const RngJump* jump;
+    const ZigTables* zig;
+    const PrimeConst* pc;                  // chain then aux
+    const u64* thr;                        // [L+2] Lemire thresholds (2^64 - q) mod q
+    int L;
+    u32 n;
+};
+
+// Set bits [lo, hi) of a shared bitmap.
+HS_DEV void set_bit_range(unsigned* bm, u32 lo, u32 hi) {
+    while (lo < hi) {
+        const u32 w = lo >> 5, b = lo & 31;
+        const u32 take = min(32u - b, hi - lo);
+        const unsigned mask = take == 32 ? 0xffffffffu : (((1u << take) - 1u) << b);
+        bm[w] |= mask;
+        lo += take;
+    }
+}
+
+constexpr double ZIG_R = 3.6541528853610088;
+constexpr double ZIG_INV_R = 0.27366123732975828;
+
+HS_DEV double next_double_of(u64 raw) { return (double)(raw >> 11) * (1.0 / 9007199254740992.0); }
+
+// Block-wide exclusive scan of a 0/1 flag (1024 threads); returns the prefix,
+// writes the block total to *total.
+HS_DEV u32 block_scan(u32 flag, u32* warp_sums, u32* total) {
+    const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned mask = __ballot_sync(0xffffffffu, flag);
+    const u32 pre = __popc(mask & ((1u << lane) - 1u));
+    if (lane == 0) warp_sums[warp] = __popc(mask);
+    __syncthreads();
+    if (warp == 0) {
+        u32 v = warp_sums[lane];
+        u32 inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            u32 t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= (u32)o) inc += t;
+        }
+        warp_sums[lane] = inc - v;
+        if (lane == 31) *total = inc;
+    }
+    __syncthreads();
+    const u32 r = warp_sums[warp] + pre;
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(RNG_T) keygen_stream_kernel(KeygenArgs A) {
+    __shared__ u64 raw[2][RNG_T];
+    __shared__ double xval[RNG_T];
+    __shared__ unsigned fastbits[RNG_T / 32];
+    __shared__ unsigned emitbits[RNG_T / 32];
+    __shared__ u32 warp_sums[32];
+    __shared__ u32 s_total;
+    __shared__ long long s_cursor;        // absolute stream position of the consumer
+    __shared__ u32 s_count;               // outputs produced in the current segment
+    __shared__ int s_seg;                 // segment index over the whole key
+    __shared__ u32 s_end;                 // chunk-relative end position of a finished segment
+
+    const int k = blockIdx.x;
+    const u32 t = threadIdx.x;
+    const int L = A.L;
+    const u32 n = A.n;
+    const int segs_per_digit = L + 3;     // (L+2) uniform + 1 normal
+    const int nseg = (L + 1) * segs_per_digit;
+    const KeyStream ks = A.streams[k];
+    const U128 inc{ks.inc_hi, ks.inc_lo};
+    const U128 AT = A.jump->A[RNG_T];
+    const U128 CT = mul128(A.jump->S[RNG_T], inc);
+    // thread t holds the state whose output is position (chunk_base + t)
+    U128 st = add128(mul128(A.jump->A[t + 1], U128{ks.state_hi, ks.state_lo}),
+                     mul128(A.jump->S[t + 1], inc));
+    u64* a_key = A.a_out[k];
+    long long* e_key = A.e_out + (size_t)k * (L + 1) * n;
+
+    // prime chunk 0 and chunk 1
+    raw[0][t] = xsl_rr(st);
+    st = add128(mul128(st, AT), CT);
+    raw[1][t] = xsl_rr(st);
+    st = add128(mul128(st, AT), CT);
+    if (t == 0) {
+        s_cursor = 0;
+        s_count = 0;
+        s_seg = 0;
+    }
+    __syncthreads();
+
+    long long chunk_base = 0;
+    int cur = 0;
+    while (true) {
+        // consume the current chunk [chunk_base, chunk_base + RNG_T)
+        while (true) {
+            const int seg = s_seg;
+            if (seg >= nseg) break;
+            const long long cursor = s_cursor;
+            if (cursor >= chunk_base + RNG_T) break;
+            const int digit = seg / segs_per_digit;
+            const int sidx = seg % segs_per_digit;
+            const u32 count0 = s_count;
+            const long long p = chunk_base + t;
+            if (sidx < L + 2) {
+                // ---- uniform segment: integers(0, q, n) by Lemire's method
+                const PrimeConst P = A.pc[sidx];
+                const u64 q = P.q;
+                const u64 thr = A.thr[sidx];
+                const u64 x = raw[cur][t];
+                const u64 lo = x * q, hi = __umul64hi(x, q);
+                const u32 acc = (p >= cursor && lo >= thr) ? 1u : 0u;
+                const u32 rank = block_scan(acc, warp_sums, &s_total);
+                const u32 idx = count0 + rank;
+                if (acc && idx < n) a_key[((size_t)digit * (L + 2) + sidx) * n + idx] = hi;
+                if (acc && idx == n - 1) s_end = t + 1;
+                __syncthreads();
+                if (t == 0) {
+                    if (count0 + s_total >= n) {
+                        s_cursor = chunk_base + s_end;
+                        s_count = 0;
+                        s_seg = seg + 1;
+                    } else {
+                        s_cursor = chunk_base + RNG_T;
+                        s_count = count0 + s_total;
+                    }
+                }
+                __syncthreads();
+            } else {
+                // ---- normal segment: 0 + 3.2 * standard_normal, rint -> int64
+                const u64 r = raw[cur][t];
+                const int zi = (int)(r & 0xff);
+                const u64 r8 = r >> 8;
+                const u64 rabs = (r8 >> 1) & 0x000fffffffffffffull;
+                double x = (double)rabs * A.zig->wi[zi];
+                if (r8 & 1) x = -x;
+                const bool fast = rabs < A.zig->ki[zi];
+                xval[t] = x;
+                const unsigned fb = __ballot_sync(0xffffffffu, fast);
+                if ((t & 31) == 0) {
+                    fastbits[t >> 5] = fb;
+                    emitbits[t >> 5] = 0u;
+                }
+                __syncthreads();
+                if (t == 0) {
+                    // token walk over [cursor, chunk end): fast tokens are 1 draw;
+                    // slow tokens need the following draw(s) (possibly next chunk)
+                    long long c = cursor;
+                    u32 cnt = count0;
+                    const long long cend = chunk_base + RNG_T;
+                    bool done = false;
+                    while (c < cend && !done) {
+                        u32 rel = (u32)(c - chunk_base);
+                        // next non-fast position at or after rel
+                        u32 s = RNG_T;
+                        for (u32 w = rel >> 5; w < RNG_T / 32; w++) {
+                            unsigned bits = ~fastbits[w];
+                            if (w == (rel >> 5)) bits &= ~((1u << (rel & 31)) - 1u);
+                            if (bits) {
+                                s = (w << 5) + __ffs(bits) - 1;
+                                break;
+                            }
+                        }
+                        u32 run = s - rel;
+                        if (cnt + run >= n) {
+                            run = n - cnt;
+                            done = true;
+                        }
+                        set_bit_range(emitbits, rel, rel + run);
+                        cnt += run;
+                        c += run;
+                        if (done || s >= RNG_T) break;
+                        // slow token at chunk position s (c == chunk_base + s)
+                        const u64 rs = raw[cur][s];
+                        const int zs = (int)(rs & 0xff);
+                        const u64 rabs_s = ((rs >> 8) >> 1) & 0x000fffffffffffffull;
+                        // draw following position c: in this chunk or the next one
+                        auto draw_at = [&](long long pos) -> u64 {
+                            const long long rp = pos - chunk_base;
+                            return rp < RNG_T ? raw[cur][rp] : raw[cur ^ 1][rp - RNG_T];
+                        };
+                        if (zs != 0) {
+                            const double xs = xval[s];
+                            const double u = next_double_of(draw_at(c + 1));
+                            const bool ok = (A.zig->fi[zs - 1] - A.zig->fi[zs]) * u + A.zig->fi[zs] <
+                                            exp(-0.5 * xs * xs);
+                            if (ok) {
+                                emitbits[s >> 5] |= 1u << (s & 31);
+                                cnt++;
+                                if (cnt >= n) done = true;
+                            }
+                            c += 2;
+                        } else {
+                            long long pos = c + 1;
+                            double v;
+                            while (true) {
+                                const double xx = -ZIG_INV_R * log1p(-next_double_of(draw_at(pos)));
+                                const double yy = -log1p(-next_double_of(draw_at(pos + 1)));
+                                pos += 2;
+                                if (yy + yy > xx * xx) {
+                                    v = ((rabs_s >> 8) & 1) ? -(ZIG_R + xx) : ZIG_R + xx;
+                                    break;
+                                }
+                            }
+                            xval[s] = v;
+                            emitbits[s >> 5] |= 1u << (s & 31);
+                            cnt++;
+                            if (cnt >= n) done = true;
+                            c = pos;
+                        }
+                    }
+                    // done: the segment's end is c (absolute)
+                    s_cursor = c;
+                    s_count = done ? n : cnt;
+                    s_end = done ? 1u : 0u;
+                }
+                __syncthreads();
+                const u32 em = (emitbits[t >> 5] >> (t & 31)) & 1u;
+                const u32 rank = block_scan(em, warp_sums, &s_total);
+                if (em) {
+                    const double v = 0.0 + 3.2 * xval[t];
+                    e_key[(size_t)digit * n + count0 + rank] = (long long)rint(v);
+                }
+                __syncthreads();
+                if (t == 0) {
+                    if (s_end) {
+                        s_count = 0;
+                        s_seg = seg + 1;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        if (s_seg >= nseg) break;
+        // advance the ring: chunk c+1 becomes current, generate chunk c+2
+        __syncthreads();
+        raw[cur][t] = xsl_rr(st);
+        st = add128(mul128(st, AT), CT);
+        cur ^= 1;
+        chunk_base += RNG_T;
+        __syncthreads();
+    }
+}
+
+// Assemble b[i][m] in place: on entry b holds NTT(e_i mod q_m); adds
+// f[i][m] * sk(X^g)_m (m <= L; sk(X^g) = NTT-domain automorphism of sk,
+// SURVEY P2) and subtracts a[i][m] * sk_m.
+__global__ void ksk_galois_kernel(Dev d, u64* const* keys, const u32* gal, const u64* sk,
+                                  const ulonglong2* f) {
+    const u32 n = d.n;
+    const u32 j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const int m = blockIdx.y % (d.L + 2), i = blockIdx.y / (d.L + 2), kk = blockIdx.z;
+    const int L = d.L;
+    const PrimeConst P = d.pc[m];
+    u64* key = keys[kk];
+    const size_t o = ((size_t)i * (L + 2) + m) * n + j;
+    u64 acc = key[o];
+    if (m <= L) {
+        const u32 src = __brev(j) >> (32 - d.log_n);
+        const u32 e = (u32)((((u64)(2 * src + 1)) * gal[kk]) & ((2ull << d.log_n) - 1));
+        const u32 pj = __brev((e - 1) >> 1) >> (32 - d.log_n);
+        const ulonglong2 w = f[i * (L + 1) + m];
+        acc = add_mod(acc, shoup(sk[(size_t)m * n + pj], w.x, w.y, P.q), P.q);
+    }
+    const u64* a = key + (size_t)(L + 1) * (L + 2) * n;
+    acc = sub_mod(acc, mul_mod(a[o], sk[(size_t)m * n + j], P), P.q);
+    key[o] = acc;
+}
+
+void keygen_streams(const Dev& d, int K, const void* streams, u64* const* a_out, long long* e_out,
+                    const void* jump, const void* zig, const u64* thr, cudaStream_t st) {
+    KeygenArgs A{(const KeyStream*)streams, a_out, e_out, (const RngJump*)jump, (const ZigTables*)zig,
+                 d.pc, thr, d.L, d.n};
+    keygen_stream_kernel<<<K, RNG_T, 0, st>>>(A);
+    note_launch();
+}
+
+void ksk_galois_combine(const Dev& d, int K, u64* const* keys, const u32* gal, const u64* sk,
+                        const ulonglong2* f, cudaStream_t st) {
+    dim3 g((d.n + 255) / 256, (d.L + 1) * (d.L + 2), K);
+    ksk_galois_kernel<<<g, 256, 0, st>>>(d, keys, gal, sk, f);
+    note_launch();
+}
+
+// b half of each key: b[i][m] = e_i mod q_m (signed coefficients)
+__global__ void e_to_limbs_kernel(Dev d, const long long* e, u64* const* keys) {
+    const u32 n = d.n;
+    const u32 j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const int m = blockIdx.y % (d.L + 2), i = blockIdx.y / (d.L + 2), kk = blockIdx.z;
+    const PrimeConst P = d.pc[m];
+    const long long c = e[((size_t)kk * (d.L + 1) + i) * n + j];
+    u64 r;
+    if (c >= 0) {
+        r = reduce64((u64)c, P);
+    } else {
+        const u64 tt = reduce64((u64)(-(c + 1)) + 1ull, P);
+        r = tt ? P.q - tt : 0ull;
+    }
+    keys[kk][((size_t)i * (d.L + 2) + m) * n + j] = r;
+}
+
+__global__ void mont_keys_kernel(Dev d, u64* const* keys) {
+    const u32 n = d.n;
+    const u32 j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const int limb = blockIdx.y, m = limb % (d.L + 2);
+    const PrimeConst P = d.pc[m];
+    u64* p = keys[blockIdx.z] + (size_t)limb * n + j;
+    *p = mont_mul(*p, P.r2_mod, P.q, P.qinv_neg);
+}
+
+// Forward NTT over the b halves of a key list (limb jb of key jb / per).
+struct JobKeyB {
+    u64* const* keys;
+    int per, L;
+    u32 n;
+    HS_DEV int prime(int jb) const { return (jb % per) % (L + 2); }
+    HS_DEV u64 load(int jb, u32 j, const PrimeConst&) const { return scratch(jb)[j]; }
+    HS_DEV u64* scratch(int jb) const { return keys[jb / per] + (size_t)(jb % per) * n; }
+    HS_DEV void store(int jb, u32 j, u64 v, const PrimeConst& P) const {
+        scratch(jb)[j] = csub(csub(v, P.two_q), P.q);
+    }
+};
+
+void keygen_assemble(const Dev& d, int K, u64* const* keys, const long long* e, const u32* gal,
+                     const u64* sk, const ulonglong2* f, cudaStream_t st) {
+    const int per = (d.L + 1) * (d.L + 2);
+    e_to_limbs_kernel<<<dim3((d.n + 255) / 256, per, K), 256, 0, st>>>(d, e, keys);
+    note_launch();
+    launch_ntt<true>(d, JobKeyB{keys, per, d.L, d.n}, K * per, st);
+    ksk_galois_combine(d, K, keys, gal, sk, f, st);
+    mont_keys_kernel<<<dim3((d.n + 255) / 256, 2 * per, K), 256, 0, st>>>(d, keys);
+    note_launch();
+}
+
+size_t rng_jump_bytes() { return sizeof(RngJump); }
+size_t zig_tables_bytes() { return sizeof(ZigTables); }
+
+}  // namespace hs
+
+// ====================================================================== host
+
+using namespace hs;
+typedef unsigned __int128 u128h;
+
+namespace {
+
+const u128h PCG_MULT = ((u128h)2549297995355413924ULL << 64) + 4865540595714422341ULL;
+
+hs_status ensure_keygen_tables(hs_ctx* c) {
+    if (c->d_jump) return HS_OK;
+    const int L = c->L;
+    RngJump* J = new RngJump();
+    u128h a = 1, s = 0;
+    for (int t = 0; t <= RNG_T; t++) {
+        J->A[t] = U128{(u64)(a >> 64), (u64)a};
+        J->S[t] = U128{(u64)(s >> 64), (u64)s};
+        s += a;
+        a *= PCG_MULT;
+    }
+    std::vector<u64> thr(L + 2);
+    for (int p = 0; p < L + 2; p++) {
+        const u64 q = c->primes[p];
+        thr[p] = (u64)((((u128h)1 << 64) - q) % q);
+    }
+    std::vector<ulonglong2> f((size_t)(L + 1) * (L + 1));
+    for (int i = 0; i <= L; i++)
+        for (int m = 0; m <= L; m++) {
+            const u64 qm = c->primes[m];
+            u64 v = c->primes[L + 1] % qm;
+            for (int j = 0; j <= L; j++)
+                if (j != i) v = (u64)((u128h)v * (c->primes[j] % qm) % qm);
+            f[(size_t)i * (L + 1) + m] = make_ulonglong2(v, (u64)(((u128h)v << 64) / qm));
+        }
+    cudaError_t e = cudaMalloc(&c->d_jump, sizeof(RngJump));
+    if (e == cudaSuccess) e = cudaMemcpy(c->d_jump, J, sizeof(RngJump), cudaMemcpyHostToDevice);
+    delete J;
+    if (e == cudaSuccess) e = cudaMalloc((void**)&c->d_thr, thr.size() * sizeof(u64));
+    if (e == cudaSuccess) e = cudaMemcpy(c->d_thr, thr.data(), thr.size() * sizeof(u64), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&c->d_kskf, f.size() * sizeof(ulonglong2));
+    if (e == cudaSuccess)
+        e = cudaMemcpy(c->d_kskf, f.data(), f.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        set_error(std::string("keygen tables: ") + cudaGetErrorString(e));
+        return HS_CUDA_ERROR;
+    }
+    return HS_OK;
+}
+
+u64 powmod_u(u64 b, u64 e, u64 q) {
+    u64 r = 1 % q;
+    b %= q;
+    while (e) {
+        if (e & 1) r = (u64)((u128h)r * b % q);
+        b = (u64)((u128h)b * b % q);
+        e >>= 1;
+    }
+    return r;
+}
+
+}  // namespace
+
+namespace hs {
+
+// Generate keys for `steps` (PCG64 start states `streams`) into `dests`
+// (each a [2][L+1][L+2][n] buffer).  Used eagerly (hs_key_generate_galois)
+// and lazily by the runner for keys it was told how to make.
+hs_status generate_galois_keys(hs_ctx* c, const std::vector<u32>& steps,
+                               const std::vector<hs_ctx::Stream>& streams,
+                               const std::vector<u64*>& dests, cudaStream_t st) {
+    if (!c->d_zig || !c->d_sk) {
+        set_error("device key generation needs hs_keygen_set_tables and hs_keygen_set_secret");
+        return HS_PARAMETER_ERROR;
+    }
+    hs_status s = ensure_keygen_tables(c);
+    if (s != HS_OK) return s;
+    const int L = c->L;
+    const u32 n = c->n;
+    const size_t half = (size_t)(L + 1) * (L + 2) * n;
+    const int KB = (int)std::max<size_t>(1, c->keygen_batch);
+    long long* e = nullptr;
+    u64** d_keys = nullptr;
+    u64** d_aout = nullptr;
+    u32* d_gal = nullptr;
+    hs_ctx::Stream* d_streams = nullptr;
+    HS_CUDA(cudaMallocAsync((void**)&e, (size_t)KB * (L + 1) * n * sizeof(long long), st));
+    HS_CUDA(cudaMallocAsync((void**)&d_keys, KB * sizeof(u64*), st));
+    HS_CUDA(cudaMallocAsync((void**)&d_aout, KB * sizeof(u64*), st));
+    HS_CUDA(cudaMallocAsync((void**)&d_gal, KB * sizeof(u32), st));
+    HS_CUDA(cudaMallocAsync((void**)&d_streams, KB * sizeof(hs_ctx::Stream), st));
+    for (size_t k0 = 0; k0 < steps.size(); k0 += KB) {
+        const int K = (int)std::min<size_t>(KB, steps.size() - k0);
+        std::vector<u64*> keys(K), aout(K);
+        std::vector<u32> gal(K);
+        for (int k = 0; k < K; k++) {
+            keys[k] = dests[k0 + k];
+            aout[k] = dests[k0 + k] + half;
+            gal[k] = (u32)powmod_u(5, steps[k0 + k], 2ull * n);
+        }
+        HS_CUDA(cudaMemcpyAsync(d_keys, keys.data(), K * sizeof(u64*), cudaMemcpyHostToDevice, st));
+        HS_CUDA(cudaMemcpyAsync(d_aout, aout.data(), K * sizeof(u64*), cudaMemcpyHostToDevice, st));
+        HS_CUDA(cudaMemcpyAsync(d_gal, gal.data(), K * sizeof(u32), cudaMemcpyHostToDevice, st));
+        HS_CUDA(cudaMemcpyAsync(d_streams, streams.data() + k0, K * sizeof(hs_ctx::Stream),
+                                cudaMemcpyHostToDevice, st));
+        keygen_streams(c->dev, K, d_streams, d_aout, e, c->d_jump, c->d_zig, c->d_thr, st);
+        keygen_assemble(c->dev, K, d_keys, e, d_gal, c->d_sk, c->d_kskf, st);
+        HS_CUDA(cudaStreamSynchronize(st));   // host staging vectors are reused
+        c->keys_generated += K;
+    }
+    cudaFreeAsync(e, st);
+    cudaFreeAsync(d_keys, st);
+    cudaFreeAsync(d_aout, st);
+    cudaFreeAsync(d_gal, st);
+    cudaFreeAsync(d_streams, st);
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) {
+        set_error(std::string("keygen launch failed: ") + cudaGetErrorString(err));
+        return HS_CUDA_ERROR;
+    }
+    return HS_OK;
+}
+
+}  // namespace hs
+
+extern "C" {
+
+hs_status hs_keygen_set_tables(hs_ctx* c, const double* wi, const double* fi, const uint64_t* ki) {
+    ZigTables z;
+    memcpy(z.wi, wi, sizeof(z.wi));
+    memcpy(z.fi, fi, sizeof(z.fi));
+    memcpy(z.ki, ki, sizeof(z.ki));
+    if (!c->d_zig) HS_CUDA(cudaMalloc(&c->d_zig, sizeof(ZigTables)));
+    HS_CUDA(cudaMemcpy(c->d_zig, &z, sizeof(z), cudaMemcpyHostToDevice));
+    return HS_OK;
+}
+
+hs_status hs_keygen_set_secret(hs_ctx* c, const uint64_t* sk_ntt, void* stream) {
+    const size_t bytes = (size_t)(c->L + 2) * c->n * sizeof(u64);
+    if (!c->d_sk) HS_CUDA(cudaMalloc((void**)&c->d_sk, bytes));
+    HS_CUDA(cudaMemcpyAsync(c->d_sk, sk_ntt, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    return HS_OK;
+}
+
+hs_status hs_keygen_register(hs_ctx* c, const uint32_t* steps, const uint64_t* states, int32_t nsteps) {
+    for (int k = 0; k < nsteps; k++) {
+        if (steps[k] == 0 || steps[k] >= c->n / 2) {
+            set_error("rotation step " + std::to_string(steps[k]) + " out of range");
+            return HS_PARAMETER_ERROR;
+        }
+        c->lazy[steps[k]] = hs_ctx::Stream{states[4 * k], states[4 * k + 1], states[4 * k + 2],
+                                           states[4 * k + 3]};
+    }
+    return HS_OK;
+}
+
+hs_status hs_key_generate_galois(hs_ctx* c, const uint32_t* steps, const uint64_t* states, int32_t nsteps,
+                                 void* stream) {
+    std::vector<u32> st(steps, steps + nsteps);
+    std::vector<hs_ctx::Stream> ss(nsteps);
+    std::vector<u64*> dests(nsteps);
+    for (int k = 0; k < nsteps; k++) {
+        if (steps[k] == 0 || steps[k] >= c->n / 2) {
+            set_error("rotation step " + std::to_string(steps[k]) + " out of range");
+            return HS_PARAMETER_ERROR;
+        }
+        ss[k] = hs_ctx::Stream{states[4 * k], states[4 * k + 1], states[4 * k + 2], states[4 * k + 3]};
+        auto it = c->galois.find(steps[k]);
+        if (it == c->galois.end()) {
+            KeyBuf kb;
+            HS_CUDA(cudaMalloc((void**)&kb.d, c->key_bytes()));
+            it = c->galois.emplace(steps[k], kb).first;
+        }
+        dests[k] = it->second.d;
+    }
+    return generate_galois_keys(c, st, ss, dests, (cudaStream_t)stream);
+}
+
+hs_status hs_keygen_streams(hs_ctx* c, const uint64_t* states, int32_t nkeys, uint64_t* a_out,
+                            int64_t* e_out, void* stream) {
+    if (!c->d_zig) {
+        set_error("hs_keygen_set_tables first");
+        return HS_PARAMETER_ERROR;
+    }
+    hs_status s = ensure_keygen_tables(c);
+    if (s != HS_OK) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t half = (size_t)(c->L + 1) * (c->L + 2) * c->n;
+    std::vector<u64*> aout(nkeys);
+    for (int k = 0; k < nkeys; k++) aout[k] = a_out + k * half;
+    u64** d_aout = nullptr;
+    void* d_streams = nullptr;
+    HS_CUDA(cudaMallocAsync((void**)&d_aout, nkeys * sizeof(u64*), st));
+    HS_CUDA(cudaMallocAsync(&d_streams, nkeys * 4 * sizeof(u64), st));
+    HS_CUDA(cudaMemcpyAsync(d_aout, aout.data(), nkeys * sizeof(u64*), cudaMemcpyHostToDevice, st));
+    HS_CUDA(cudaMemcpyAsync(d_streams, states, nkeys * 4 * sizeof(u64), cudaMemcpyHostToDevice, st));
+    keygen_streams(c->dev, nkeys, d_streams, d_aout, (long long*)e_out, c->d_jump, c->d_zig, c->d_thr, st);
+    HS_CUDA(cudaStreamSynchronize(st));
+    cudaFreeAsync(d_aout, st);
+    cudaFreeAsync(d_streams, st);
+    return HS_OK;
+}
+
+}  // extern "C"
+
+extern "C" int64_t hs_keys_generated(const hs_ctx* c) { return c->keys_generated; }

@@ -80,6 +80,12 @@ void encrypt_combine(const Dev& d, int nl, const u64* v, const u64* pkb, const u
 // Decrypt: pt[i] = c0[i] + c1[i] s[i]
 void decrypt_combine(const Dev& d, int nl, const u64* ct, const u64* sk, u64* pt, cudaStream_t st);
 
+// ---- on-device Galois key generation (keygen.cu)
+void keygen_streams(const Dev& d, int K, const void* streams, u64* const* a_out, long long* e_out,
+                    const void* jump, const void* zig, const u64* thr, cudaStream_t st);
+void keygen_assemble(const Dev& d, int K, u64* const* keys, const long long* e, const u32* gal,
+                     const u64* sk, const ulonglong2* f, cudaStream_t st);
+
 // data[i] mod q for limbs after an integer-sum collective
 void reduce_mod(const Dev& d, u64* data, int npoly, int nl, cudaStream_t st);
 

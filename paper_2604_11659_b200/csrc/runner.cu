@@ -97,6 +97,61 @@ struct DeviceArena {
     }
 };
 
+// Galois keys for a set of steps: resident keys from the context store, or
+// keys generated on the device on demand (steps registered with
+// hs_keygen_register), owned here and freed when no longer needed.
+struct KeyProvider {
+    hs_ctx* c;
+    cudaStream_t st;
+    std::unordered_map<u32, u64*> temp;
+    ~KeyProvider() {
+        for (auto& kv : temp) cudaFreeAsync(kv.second, st);
+    }
+    bool needs_generation(u32 r) const { return !c->galois.count(r) && !temp.count(r); }
+    void release_except(const std::vector<u32>& keep) {
+        for (auto it = temp.begin(); it != temp.end();) {
+            if (std::find(keep.begin(), keep.end(), it->first) == keep.end()) {
+                cudaFreeAsync(it->second, st);
+                it = temp.erase(it);
+            } else {
+                ++it;
+            }
+        }
+    }
+    hs_status get(const std::vector<u32>& steps, std::vector<const u64*>& out) {
+        std::vector<u32> gen;
+        std::vector<hs_ctx::Stream> ss;
+        std::vector<u64*> dst;
+        for (u32 r : steps) {
+            if (!needs_generation(r) || std::find(gen.begin(), gen.end(), r) != gen.end()) continue;
+            auto lz = c->lazy.find(r);
+            if (lz == c->lazy.end()) {
+                set_error("missing Galois key for step " + std::to_string(r));
+                return HS_KEY_MISSING;
+            }
+            u64* buf = nullptr;
+            if (cudaMallocAsync((void**)&buf, c->key_bytes(), st) != cudaSuccess) {
+                set_error("out of device memory for generated Galois keys");
+                return HS_OUT_OF_MEMORY;
+            }
+            temp[r] = buf;
+            gen.push_back(r);
+            ss.push_back(lz->second);
+            dst.push_back(buf);
+        }
+        if (!gen.empty()) {
+            hs_status s = generate_galois_keys(c, gen, ss, dst, st);
+            if (s != HS_OK) return s;
+        }
+        out.resize(steps.size());
+        for (size_t k = 0; k < steps.size(); k++) {
+            auto it = c->galois.find(steps[k]);
+            out[k] = it != c->galois.end() ? it->second.d : temp[steps[k]];
+        }
+        return HS_OK;
+    }
+};
+
 hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, const u64* ct_a,
                     const u64* ct_b, const u64* const* masks, int64_t nmasks, u64* out,
                     hs_counters* cnt, int shard, int nshard, cudaStream_t st,
@@ -123,11 +178,10 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, cons
     std::vector<std::pair<int, u32>> align_list;     // (src, r)
     auto galois_key = [&](int64_t raw, u32 r) -> const u64* {
         auto it = c->galois.find(r);
-        if (it == c->galois.end()) {
-            set_error("missing Galois key for step " + std::to_string(raw));
-            return nullptr;
-        }
-        return it->second.d;
+        if (it != c->galois.end()) return it->second.d;
+        if (c->lazy.count(r)) return (const u64*)1;     // generated on demand
+        set_error("missing Galois key for step " + std::to_string(raw));
+        return nullptr;
     };
     if (!c->relin.d && np) {
         set_error("no relinearization key in bundle");
@@ -214,7 +268,10 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, cons
     }
 
     DeviceArena A{st};
+    KeyProvider KP{c, st, {}};
     const size_t budget = c->batch_bytes;
+    // generated keys per chunk/batch are bounded by twice the work budget
+    const int64_t max_gen = std::max<int64_t>(1, (int64_t)(2 * budget / c->key_bytes()));
 
     // ---- phase 1: hoisted alignment rotations
     u64* aligned = A.get<u64>(need.size() * ctL);
@@ -223,22 +280,26 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, cons
         return (hs_status)HS_OUT_OF_MEMORY;
     }
     for (int src = 0; src < 2; src++) {
-        std::vector<u32> gal;
+        std::vector<u32> gal, steps_src;
         std::vector<const u64*> keys;
         std::vector<const u64*> outs;
         for (size_t k = 0; k < need.size(); k++) {
             const auto& al = align_list[need[k] - 2];
             if (al.first != src) continue;
             gal.push_back((u32)powmod_h(5, al.second, 2ull * n));
-            keys.push_back(c->galois[al.second].d);
+            steps_src.push_back(al.second);
             outs.push_back(aligned + k * ctL);
         }
+        keys.assign(gal.size(), nullptr);
         const int R = (int)gal.size();
         if (!R) continue;
         const size_t base_e = ks_hoisted_scratch_elems(0, L, n);
         const size_t per_e = ks_hoisted_scratch_elems(1, L, n) - base_e;
         int64_t rmax = budget / 8 > base_e ? (int64_t)((budget / 8 - base_e) / per_e) : 1;
         rmax = std::max<int64_t>(1, std::min<int64_t>(rmax, R));
+        bool any_gen = false;
+        for (u32 r : steps_src) any_gen |= KP.needs_generation(r);
+        if (any_gen) rmax = std::min<int64_t>(rmax, max_gen);
         u64* scratch = A.get<u64>(ks_hoisted_scratch_elems((int)rmax, L, n));
         u32* d_gal = A.get<u32>(R);
         const u64** d_keys = A.get<const u64*>(R);
@@ -248,12 +309,18 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, cons
             return (hs_status)HS_OUT_OF_MEMORY;
         }
         HS_CUDA(cudaMemcpyAsync(d_gal, gal.data(), R * sizeof(u32), cudaMemcpyHostToDevice, st));
-        HS_CUDA(cudaMemcpyAsync(d_keys, keys.data(), R * sizeof(u64*), cudaMemcpyHostToDevice, st));
         HS_CUDA(cudaMemcpyAsync(d_outs, outs.data(), R * sizeof(u64*), cudaMemcpyHostToDevice, st));
         const u64* sp = src ? ct_b : ct_a;
         for (int r0 = 0; r0 < R; r0 += (int)rmax) {
             const int rc = std::min<int>((int)rmax, R - r0);
+            std::vector<u32> chunk(steps_src.begin() + r0, steps_src.begin() + r0 + rc);
+            std::vector<const u64*> kp;
+            KP.release_except(chunk);
+            hs_status ks_ = KP.get(chunk, kp);
+            if (ks_ != HS_OK) return ks_;
+            HS_CUDA(cudaMemcpyAsync(d_keys + r0, kp.data(), rc * sizeof(u64*), cudaMemcpyHostToDevice, st));
             rotate_hoisted(d, rc, L, sp, d_gal + r0, d_keys + r0, table(d_outs + r0), scratch, st);
+            if (any_gen) HS_CUDA(cudaStreamSynchronize(st));   // kp staging
         }
     }
 
@@ -265,7 +332,6 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, cons
         hA[t] = ia[p] >= 2 ? aligned + (size_t)slot_of[ia[p]] * ctL : ct_a;
         hB[t] = ib[p] >= 2 ? aligned + (size_t)slot_of[ib[p]] * ctL : ct_b;
         hM[t] = masks[mpos[p]];
-        hK[t] = accr[p] ? c->galois[accr[p]].d : nullptr;
         hG[t] = accr[p] ? (u32)powmod_h(5, accr[p], 2ull * n) : 0u;
     }
     const size_t per_pair = ks_scratch_elems(1, L, n) +
@@ -292,12 +358,35 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, cons
     HS_CUDA(cudaMemcpyAsync(dA, hA.data(), P * sizeof(u64*), cudaMemcpyHostToDevice, st));
     HS_CUDA(cudaMemcpyAsync(dB, hB.data(), P * sizeof(u64*), cudaMemcpyHostToDevice, st));
     HS_CUDA(cudaMemcpyAsync(dM, hM.data(), P * sizeof(u64*), cudaMemcpyHostToDevice, st));
-    HS_CUDA(cudaMemcpyAsync(dK, hK.data(), P * sizeof(u64*), cudaMemcpyHostToDevice, st));
     HS_CUDA(cudaMemcpyAsync(dG, hG.data(), P * sizeof(u32), cudaMemcpyHostToDevice, st));
     HS_CUDA(cudaMemcpyAsync(dR, relin_rep.data(), B * sizeof(u64*), cudaMemcpyHostToDevice, st));
 
-    for (int64_t s = 0; s < P; s += B) {
-        const int bn = (int)std::min<int64_t>(B, P - s);
+    std::vector<u32> hR(P);
+    for (int64_t t = 0; t < P; t++) hR[t] = accr[order[lo + t]];
+    for (int64_t s = 0, bnext; s < P; s = bnext) {
+        // batch: up to B pairs, and at most max_gen distinct keys still to generate
+        std::vector<u32> bsteps;
+        int64_t ngen = 0;
+        bnext = s;
+        while (bnext < P && bnext - s < B) {
+            const u32 r = hR[bnext];
+            if (r && (bsteps.empty() || bsteps.back() != r)) {
+                if (KP.needs_generation(r) && ngen + 1 > max_gen && bnext > s) break;
+                bsteps.push_back(r);
+                if (KP.needs_generation(r)) ngen++;
+            }
+            bnext++;
+        }
+        const int bn = (int)(bnext - s);
+        KP.release_except(bsteps);
+        std::vector<const u64*> bkeys;
+        hs_status ks_ = KP.get(bsteps, bkeys);
+        if (ks_ != HS_OK) return ks_;
+        for (int64_t t = s, k = -1; t < bnext; t++) {
+            if (hR[t] && (k < 0 || bsteps[k] != hR[t])) k++;
+            hK[t] = hR[t] ? bkeys[k] : nullptr;
+        }
+        HS_CUDA(cudaMemcpyAsync(dK + s, hK.data() + s, bn * sizeof(u64*), cudaMemcpyHostToDevice, st));
         int z = 0;
         while (z < bn && hG[s + z] == 0) z++;
         // mult_ct + relinearize (fused), level L
@@ -316,6 +405,7 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, cons
                          strided(Fb + (size_t)z * ctL2, ctL2), ks, st);
         accumulate(d, z, L - 1, 2, strided(Cb, ctL2), out, st);
         accumulate(d, bn - z, L - 1, 2, strided(Fb + (size_t)z * ctL2, ctL2), out, st);
+        if (ngen) HS_CUDA(cudaStreamSynchronize(st));   // generated keys are freed next batch
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {

@@ -212,6 +212,28 @@ def main():
     for c in cases:
         meta["runner"]["_".join(str(x) for x in c)] = run_case(*c)
 
+    # 5. plaintext schedules of all four runners (encmat.py:150-251) + predicted counts
+    from hespmm.encmat import meta_and_values
+    from hespmm.engine import MatmulMethod as MM
+    from hespmm.oracle import predicted_op_counts
+    meta["schedules"] = {}
+    for dim, sp, mseed in [(4, 0.3, 51), (8, 0.5, 4), (12, 0.75, 9), (16, 0.9, 2)]:
+        a = generate_random_sparse(dim, sp, (mseed, 0))
+        b = generate_random_sparse(dim, sp, (mseed, 1))
+        for method, la, lb, skip in [(MM.CSR_C, Layout.CSR, Layout.CSC, None),
+                                     (MM.VCSR_C, Layout.VCSR, Layout.VCSC, None),
+                                     (MM.NAIVE_DENSE, Layout.DENSE_ROW_MAJOR, Layout.DENSE_COL_MAJOR, None),
+                                     (MM.NAIVE_SPARSE, Layout.DENSE_ROW_MAJOR, Layout.DENSE_COL_MAJOR, "either")]:
+            ma, va = meta_and_values(a, la)
+            mb, vb = meta_and_values(b, lb)
+            pairs = np.array(list(pair_schedule(ma, mb, skip=skip)), dtype=np.int64).reshape(-1, 4)
+            pred = predicted_op_counts(a, b, method)
+            meta["schedules"][f"{dim}_{sp}_{mseed}_{method.value}"] = {
+                "pairs": h(pairs.astype(np.uint64)), "npairs": len(pairs),
+                "steps": sorted(required_rotation_steps(ma, mb, skip=skip)),
+                "values_a": h(np.asarray(va).view(np.uint64)), "values_b": h(np.asarray(vb).view(np.uint64)),
+                "pred": [pred.matching_pairs, pred.alignment_rotations, pred.accumulation_rotations]}
+
     np.savez_compressed(os.path.join(HERE, "golden_small.npz"), **small)
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(meta, fh, indent=1, sort_keys=True)
