@@ -44,6 +44,15 @@ WORKLOADS = {
                  desc="configs[1]: N=2^14, 64x64 @75% sparsity, single B200"),
     "cfg1": dict(ring_degree=1 << 10, scale_bits=45, levels=2, seed=2024, dim=16, sparsity=0.5,
                  desc="configs[0]: desk-small params (pkg/params), 16x16 @50%"),
+    # configs[2]: N=2^16, L=24; 12,956 Galois keys (8.8 TB) are generated on
+    # the device on demand inside the timed step (they cannot be stored).
+    "cfg3": dict(ring_degree=1 << 16, scale_bits=50, levels=24, seed=2024, dim=128, sparsity=0.9,
+                 lazy_keys=True, batch_gb=16,
+                 desc="configs[2]: N=2^16, L=24, 128x128 @90%, hoisted rotations, "
+                      "Galois keys generated on device inside the step"),
+    "cfg3s": dict(ring_degree=1 << 16, scale_bits=50, levels=24, seed=2024, dim=32, sparsity=0.9,
+                  lazy_keys=True, batch_gb=16,
+                  desc="N=2^16, L=24, 32x32 @90% (cfg3 parameters, smaller matrix)"),
 }
 
 
@@ -122,7 +131,10 @@ def make_inputs(pkg, wl):
     ea = encmat.encrypt_sparse(a, encmat.Layout.CSR, ctx, keys)
     eb = encmat.encrypt_sparse(b, encmat.Layout.CSC, ctx, keys)
     steps = encmat.required_rotation_steps(ea.meta, eb.meta)
-    keys = ctx.gen_galois_keys(steps, keys)
+    keys = ctx.gen_galois_keys(steps, keys, device="lazy" if wl.get("lazy_keys") else False)
+    if wl.get("batch_gb"):
+        from paper_2604_11659_b200._lib import lib
+        lib().hs_set_batch_bytes(ctx.handle, int(wl["batch_gb"]) << 30)
     pairs = encmat.pair_array(ea.meta, eb.meta)
     mc = engine.MaskCache(ctx, wl["dim"])
     mc.prewarm(np.unique(np.minimum(pairs[:, 2], pairs[:, 3])))

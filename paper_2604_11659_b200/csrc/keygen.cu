@@ -385,11 +385,18 @@ struct JobKeyB {
     u64* const* keys;
     int per, L;
     u32 n;
-    HS_DEV int prime(int jb) const { return (jb % per) % (L + 2); }
-    HS_DEV u64 load(int jb, u32 j, const PrimeConst&) const { return scratch(jb)[j]; }
-    HS_DEV u64* scratch(int jb) const { return keys[jb / per] + (size_t)(jb % per) * n; }
-    HS_DEV void store(int jb, u32 j, u64 v, const PrimeConst& P) const {
-        scratch(jb)[j] = csub(csub(v, P.two_q), P.q);
+    struct Ctx {
+        u64* limb;
+        int p;
+    };
+    HS_DEV Ctx make(int jb) const {
+        return Ctx{keys[jb / per] + (size_t)(jb % per) * n, (jb % per) % (L + 2)};
+    }
+    HS_DEV int prime(const Ctx& c) const { return c.p; }
+    HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst&) const { return c.limb[j]; }
+    HS_DEV u64* scratch(const Ctx& c) const { return c.limb; }
+    HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst& P) const {
+        c.limb[j] = csub(csub(v, P.two_q), P.q);
     }
 };
 

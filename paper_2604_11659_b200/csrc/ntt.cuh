@@ -37,7 +37,9 @@ HS_DEV u32 spad(u32 i) { return i + (i >> 3); }
 
 // One register round: local stages [A, A+R) of a tile with H rows, G = 2^LOGG
 // group elements and C columns.  A "unit" is the 2^R elements that differ in
-// the round's bits; each thread owns 8 / 2^R units, 8 elements in registers.
+// the round's bits (smem stride S = 2^LOWB * C); each thread owns 8 / 2^R
+// units.  The round schedule (ntt_rounds_*) keeps LOWB = 0 or LOWB >= 3, so
+// the padded smem index of a unit's elements is affine: base + e * PS.
 template <bool FWD, int LOGG, int H, int C, int A, int R>
 __device__ __forceinline__ void ntt_round(u64* sm, const ulonglong2* __restrict__ tw, u32 hi0,
                                           int s0, u64 q, u64 two_q) {
@@ -47,6 +49,9 @@ __device__ __forceinline__ void ntt_round(u64* sm, const ulonglong2* __restrict_
     constexpr int NU = 1 << R;
     constexpr int UPT = NTT_EPT / NU;
     constexpr int LOWB = LOGG - A - R;
+    constexpr int S = (1 << LOWB) * C;
+    static_assert(S % 8 == 0 || (S == 1 && R == 3), "round schedule must keep smem affine");
+    constexpr int PS = S % 8 == 0 ? S + S / 8 : 1;
 #pragma unroll
     for (int k = 0; k < UPT; k++) {
         const u32 U = threadIdx.x + k * T;
@@ -58,22 +63,21 @@ __device__ __forceinline__ void ntt_round(u64* sm, const ulonglong2* __restrict_
         const u32 go_low = go & ((1u << LOWB) - 1);
         const u32 gbase = (go_high << (LOWB + R)) | go_low;
         const u32 hi = hi0 + h;
+        const u32 base = spad((h * G + gbase) * C + c);
         u64 v[NU];
 #pragma unroll
-        for (int e = 0; e < NU; e++) v[e] = sm[spad((h * G + (gbase | ((u32)e << LOWB))) * C + c)];
+        for (int e = 0; e < NU; e++) v[e] = sm[base + e * PS];
         if (FWD) {
 #pragma unroll
             for (int j = 0; j < R; j++) {
                 const int ls = A + j;
-                const u32 base = (1u << (s0 + ls)) + (hi << ls) + (go_high << j);
-                constexpr int dummy = 0;
-                (void)dummy;
+                const u32 tb = (1u << (s0 + ls)) + (hi << ls) + (go_high << j);
 #pragma unroll
                 for (int e = 0; e < NU; e++) {
                     const int bit = 1 << (R - 1 - j);
                     if (e & bit) continue;
-                    const ulonglong2 w = tw[base + (e >> (R - j))];
-                    u64 x = csub(v[e], two_q);
+                    const ulonglong2 w = tw[tb + (e >> (R - j))];
+                    const u64 x = csub(v[e], two_q);
                     const u64 t = shoup_lazy(v[e + bit], w.x, w.y, q);
                     v[e] = x + t;
                     v[e + bit] = x - t + two_q;
@@ -83,12 +87,12 @@ __device__ __forceinline__ void ntt_round(u64* sm, const ulonglong2* __restrict_
 #pragma unroll
             for (int j = R - 1; j >= 0; j--) {
                 const int ls = A + j;
-                const u32 base = (1u << (s0 + ls)) + (hi << ls) + (go_high << j);
+                const u32 tb = (1u << (s0 + ls)) + (hi << ls) + (go_high << j);
 #pragma unroll
                 for (int e = 0; e < NU; e++) {
                     const int bit = 1 << (R - 1 - j);
                     if (e & bit) continue;
-                    const ulonglong2 w = tw[base + (e >> (R - j))];
+                    const ulonglong2 w = tw[tb + (e >> (R - j))];
                     const u64 x = v[e], y = v[e + bit];
                     v[e] = csub(x + y, two_q);
                     v[e + bit] = shoup_lazy(x - y + two_q, w.x, w.y, q);
@@ -96,44 +100,73 @@ __device__ __forceinline__ void ntt_round(u64* sm, const ulonglong2* __restrict_
             }
         }
 #pragma unroll
-        for (int e = 0; e < NU; e++) sm[spad((h * G + (gbase | ((u32)e << LOWB))) * C + c)] = v[e];
+        for (int e = 0; e < NU; e++) sm[base + e * PS] = v[e];
     }
 }
 
-template <int LOGG, int H, int C, int A>
-__device__ __forceinline__ void ntt_rounds_fwd(u64* sm, const ulonglong2* tw, u32 hi0, int s0,
-                                               u64 q, u64 two_q) {
-    if constexpr (A < LOGG) {
-        constexpr int R = (LOGG - A) < 3 ? (LOGG - A) : 3;
-        ntt_round<true, LOGG, H, C, A, R>(sm, tw, hi0, s0, q, two_q);
+// Round schedule: radix-8 rounds, the remainder (LOGG mod 3) as the
+// second-to-last round, so the last (lowest-bit) round is always radix 8.
+template <int LOGG>
+struct RoundPlan {
+    static constexpr int F = LOGG / 3, REM = LOGG % 3;
+    // start stage and width of round number r (0-based, forward order)
+    static constexpr int count() { return F + (REM ? 1 : 0); }
+    static constexpr int start(int r) {
+        return REM == 0 ? 3 * r : (r < F - 1 ? 3 * r : (r == F - 1 ? 3 * (F - 1) : LOGG - 3));
+    }
+    static constexpr int width(int r) { return REM == 0 ? 3 : (r == F - 1 ? REM : 3); }
+};
+
+template <int LOGG, int H, int C, int RI>
+__device__ __forceinline__ void ntt_rounds_fwd_from(u64* sm, const ulonglong2* tw, u32 hi0, int s0,
+                                                    u64 q, u64 two_q) {
+    if constexpr (RI < RoundPlan<LOGG>::count()) {
+        ntt_round<true, LOGG, H, C, RoundPlan<LOGG>::start(RI), RoundPlan<LOGG>::width(RI)>(
+            sm, tw, hi0, s0, q, two_q);
         __syncthreads();
-        ntt_rounds_fwd<LOGG, H, C, A + R>(sm, tw, hi0, s0, q, two_q);
+        ntt_rounds_fwd_from<LOGG, H, C, RI + 1>(sm, tw, hi0, s0, q, two_q);
     }
 }
 
-template <int LOGG, int H, int C, int TOP>
-__device__ __forceinline__ void ntt_rounds_inv(u64* sm, const ulonglong2* tw, u32 hi0, int s0,
-                                               u64 q, u64 two_q) {
-    if constexpr (TOP > 0) {
-        constexpr int R = TOP < 3 ? TOP : 3;
-        ntt_round<false, LOGG, H, C, TOP - R, R>(sm, tw, hi0, s0, q, two_q);
+template <int LOGG, int H, int C, int RI>
+__device__ __forceinline__ void ntt_rounds_inv_from(u64* sm, const ulonglong2* tw, u32 hi0, int s0,
+                                                    u64 q, u64 two_q) {
+    if constexpr (RI >= 0) {
+        ntt_round<false, LOGG, H, C, RoundPlan<LOGG>::start(RI), RoundPlan<LOGG>::width(RI)>(
+            sm, tw, hi0, s0, q, two_q);
         __syncthreads();
-        ntt_rounds_inv<LOGG, H, C, TOP - R>(sm, tw, hi0, s0, q, two_q);
+        ntt_rounds_inv_from<LOGG, H, C, RI - 1>(sm, tw, hi0, s0, q, two_q);
     }
 }
 
+template <int LOGG, int H, int C>
+__device__ __forceinline__ void ntt_rounds_fwd(u64* sm, const ulonglong2* tw, u32 hi0, int s0, u64 q,
+                                               u64 two_q) {
+    ntt_rounds_fwd_from<LOGG, H, C, 0>(sm, tw, hi0, s0, q, two_q);
+}
+
+template <int LOGG, int H, int C>
+__device__ __forceinline__ void ntt_rounds_inv(u64* sm, const ulonglong2* tw, u32 hi0, int s0, u64 q,
+                                               u64 two_q) {
+    ntt_rounds_inv_from<LOGG, H, C, RoundPlan<LOGG>::count() - 1>(sm, tw, hi0, s0, q, two_q);
+}
+
+// Job interface: `typename Job::Ctx ctx = job.make(jb)` is evaluated once per
+// CTA (pointer-table lookups, index decoding), then prime(ctx),
+// load(ctx, j, P), scratch(ctx), store(ctx, j, v, P) per element.
 template <bool FWD, bool FIRST, bool LAST, int LOGG, int H, int C, class Job>
 __global__ void __launch_bounds__(NTT_THREADS)
 ntt_pass_kernel(Dev d, Job job, int s0, int jbase) {
     constexpr int G = 1 << LOGG;
     constexpr int TILE = H * G * C;
+    constexpr int T = TILE / NTT_EPT;
     __shared__ u64 sm[TILE + TILE / 8];
 
     const int log_n = d.log_n;
-    const int s1 = s0 + LOGG;
-    const int lo_bits = log_n - s1;
+    const int lo_bits = log_n - s0 - LOGG;
     const int jb = jbase + (int)blockIdx.y;
-    const int p = job.prime(jb);
+    const typename Job::Ctx jc = job.make(jb);
+    const int p = job.prime(jc);
     const PrimeConst P = d.pc[p];
     const ulonglong2* __restrict__ tw = (FWD ? d.tw : d.itw) + (size_t)p * d.n;
 
@@ -141,26 +174,34 @@ ntt_pass_kernel(Dev d, Job job, int s0, int jbase) {
     const u32 hi0 = (blockIdx.x / ncolblk) * H;
     const u32 lo0 = (blockIdx.x % ncolblk) * C;
 
+    // element e = t + k*T of the tile sits at global index j0 + k*jstep
     auto gidx = [&](u32 e) -> u32 {
         u32 c = e % C, g = (e / C) % G, h = e / (C * G);
         return ((hi0 + h) << (log_n - s0)) | (g << lo_bits) | (lo0 + c);
     };
+    const u32 t = threadIdx.x;
+    const u32 j0 = gidx(t);
+    const u32 jstep = NTT_EPT > 1 ? gidx(t + T) - j0 : 0;
 
     if (FIRST) {
-        for (u32 e = threadIdx.x; e < TILE; e += blockDim.x) sm[spad(e)] = job.load(jb, gidx(e), P);
+#pragma unroll
+        for (int k = 0; k < NTT_EPT; k++) sm[spad(t + k * T)] = job.load(jc, j0 + k * jstep, P);
     } else {
-        const u64* __restrict__ src = job.scratch(jb);
-        for (u32 e = threadIdx.x; e < TILE; e += blockDim.x) sm[spad(e)] = src[gidx(e)];
+        const u64* __restrict__ src = job.scratch(jc);
+#pragma unroll
+        for (int k = 0; k < NTT_EPT; k++) sm[spad(t + k * T)] = src[j0 + k * jstep];
     }
     __syncthreads();
-    if (FWD) ntt_rounds_fwd<LOGG, H, C, 0>(sm, tw, hi0, s0, P.q, P.two_q);
-    else ntt_rounds_inv<LOGG, H, C, LOGG>(sm, tw, hi0, s0, P.q, P.two_q);
+    if (FWD) ntt_rounds_fwd<LOGG, H, C>(sm, tw, hi0, s0, P.q, P.two_q);
+    else ntt_rounds_inv<LOGG, H, C>(sm, tw, hi0, s0, P.q, P.two_q);
 
     if (LAST) {
-        for (u32 e = threadIdx.x; e < TILE; e += blockDim.x) job.store(jb, gidx(e), sm[spad(e)], P);
+#pragma unroll
+        for (int k = 0; k < NTT_EPT; k++) job.store(jc, j0 + k * jstep, sm[spad(t + k * T)], P);
     } else {
-        u64* __restrict__ dst = job.scratch(jb);
-        for (u32 e = threadIdx.x; e < TILE; e += blockDim.x) dst[gidx(e)] = sm[spad(e)];
+        u64* __restrict__ dst = job.scratch(jc);
+#pragma unroll
+        for (int k = 0; k < NTT_EPT; k++) dst[j0 + k * jstep] = sm[spad(t + k * T)];
     }
 }
 

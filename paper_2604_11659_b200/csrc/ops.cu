@@ -65,6 +65,7 @@ HS_DEV u32 galois_perm(u32 k, u32 g, int log_n) {
 }
 
 // =========================================================== plain NTT jobs
+// Job interface (ntt.cuh): Ctx make(jb) once per CTA; prime/load/scratch/store.
 
 template <bool FWD>
 struct JobPlain {
@@ -72,13 +73,19 @@ struct JobPlain {
     const u64* src;     // optional separate source (same layout) or nullptr
     PrimeMap pm;
     u32 n;
-    HS_DEV int prime(int jb) const { return pm.p[jb % pm.nl]; }
-    HS_DEV u64 load(int jb, u32 j, const PrimeConst&) const {
-        return (src ? src : buf)[(size_t)jb * n + j];
+    struct Ctx {
+        const u64* src;
+        u64* dst;
+        int p;
+    };
+    HS_DEV Ctx make(int jb) const {
+        return Ctx{(src ? src : buf) + (size_t)jb * n, buf + (size_t)jb * n, pm.p[jb % pm.nl]};
     }
-    HS_DEV u64* scratch(int jb) const { return buf + (size_t)jb * n; }
-    HS_DEV void store(int jb, u32 j, u64 v, const PrimeConst& P) const {
-        buf[(size_t)jb * n + j] = FWD ? canon4(v, P) : shoup(v, P.n_inv, P.n_inv_sh, P.q);
+    HS_DEV int prime(const Ctx& c) const { return c.p; }
+    HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst&) const { return c.src[j]; }
+    HS_DEV u64* scratch(const Ctx& c) const { return c.dst; }
+    HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst& P) const {
+        c.dst[j] = FWD ? canon4(v, P) : shoup(v, P.n_inv, P.n_inv_sh, P.q);
     }
 };
 
@@ -95,14 +102,19 @@ struct JobInvGather {
     int npoly, nl, limb, prime_idx;
     u64* dst;           // [jobs][n]
     u32 n;
-    HS_DEV int prime(int) const { return prime_idx; }
-    HS_DEV u64 load(int jb, u32 j, const PrimeConst&) const {
-        int b = jb / npoly, poly = jb % npoly;
-        return in.at(b)[((size_t)poly * nl + limb) * n + j];
+    struct Ctx {
+        const u64* src;
+        u64* dst;
+    };
+    HS_DEV Ctx make(int jb) const {
+        const int b = jb / npoly, poly = jb % npoly;
+        return Ctx{in.at(b) + ((size_t)poly * nl + limb) * n, dst + (size_t)jb * n};
     }
-    HS_DEV u64* scratch(int jb) const { return dst + (size_t)jb * n; }
-    HS_DEV void store(int jb, u32 j, u64 v, const PrimeConst& P) const {
-        dst[(size_t)jb * n + j] = shoup(v, P.n_inv, P.n_inv_sh, P.q);
+    HS_DEV int prime(const Ctx&) const { return prime_idx; }
+    HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst&) const { return c.src[j]; }
+    HS_DEV u64* scratch(const Ctx& c) const { return c.dst; }
+    HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst& P) const {
+        c.dst[j] = shoup(v, P.n_inv, P.n_inv_sh, P.q);
     }
 };
 
@@ -114,26 +126,44 @@ struct JobInvGather {
 //   ACC [B][2][l+2][n]    key inner products (b then a component).
 //   T   [B][2][n]         INTT of ACC aux limbs.
 
-// Digit sources: the NTT-domain limb x_i that is decomposed.
-struct SrcPlain {      // x = ct(b).c1[i]   (relin of a stored d2 uses poly_off 2)
+// Digit sources: the NTT-domain limb x_i that is decomposed (bound per CTA).
+struct SrcPlain {      // x = ct(b).poly[i]
     ItemPtr ct;
-    int poly;          // which poly holds x
-    HS_DEV u64 x(int b, int i, int l, u32 j, u32 n, const Dev&, const PrimeConst&) const {
-        return ct.at(b)[((size_t)poly * (l + 1) + i) * n + j];
+    int poly;
+    struct B {
+        const u64* x;
+    };
+    HS_DEV B bind(int b, int i, int l, u32 n, const Dev&) const {
+        return B{ct.at(b) + ((size_t)poly * (l + 1) + i) * n};
     }
+    HS_DEV u64 x(const B& s, u32 j, const Dev&, const PrimeConst&) const { return s.x[j]; }
 };
 struct SrcPerm {       // x = automorphism_g(ct(b).c1)[i]
     ItemPtr ct;
-    const u32* gal;    // per item Galois element
-    HS_DEV u64 x(int b, int i, int l, u32 j, u32 n, const Dev& d, const PrimeConst&) const {
-        return ct.at(b)[((size_t)(l + 1) + i) * n + galois_perm(j, gal[b], d.log_n)];
+    const u32* gal;
+    struct B {
+        const u64* x;
+        u32 g;
+    };
+    HS_DEV B bind(int b, int i, int l, u32 n, const Dev&) const {
+        return B{ct.at(b) + ((size_t)(l + 1) + i) * n, gal[b]};
+    }
+    HS_DEV u64 x(const B& s, u32 j, const Dev& d, const PrimeConst&) const {
+        return s.x[galois_perm(j, s.g, d.log_n)];
     }
 };
 struct SrcTensor {     // x = d2 = a1 * b1 of the tensor product of two cts
     ItemPtr a, bb;
-    HS_DEV u64 x(int b, int i, int l, u32 j, u32 n, const Dev&, const PrimeConst& P) const {
-        size_t o = ((size_t)(l + 1) + i) * n + j;
-        return mul_mod(a.at(b)[o], bb.at(b)[o], P);
+    struct B {
+        const u64* a;
+        const u64* b;
+    };
+    HS_DEV B bind(int b, int i, int l, u32 n, const Dev&) const {
+        const size_t o = ((size_t)(l + 1) + i) * n;
+        return B{a.at(b) + o, bb.at(b) + o};
+    }
+    HS_DEV u64 x(const B& s, u32 j, const Dev&, const PrimeConst& P) const {
+        return mul_mod(s.a[j], s.b[j], P);
     }
 };
 
@@ -146,18 +176,27 @@ struct JobDecompose {                       // inverse NTT, job = b*(l+1)+i
     int l;
     u32 n;
     Dev d;
-    HS_DEV int prime(int jb) const { return jb % (l + 1); }
-    HS_DEV u64 load(int jb, u32 j, const PrimeConst& P) const {
-        int b = jb / (l + 1), i = jb % (l + 1);
-        u64 x = src.x(b, i, l, j, n, d, P);
-        ulonglong2 w = df[i];
-        u64 v = shoup(x, w.x, w.y, P.q);
-        E[((size_t)jb * (l + 2) + i) * n + j] = v;
+    struct Ctx {
+        typename Src::B s;
+        u64* e;              // E[b][i][i]
+        u64* dd;             // D[b][i]
+        ulonglong2 w;        // digit factor
+        int i;
+    };
+    HS_DEV Ctx make(int jb) const {
+        const int b = jb / (l + 1), i = jb % (l + 1);
+        return Ctx{src.bind(b, i, l, n, d), E + ((size_t)jb * (l + 2) + i) * n, D + (size_t)jb * n,
+                   df[i], i};
+    }
+    HS_DEV int prime(const Ctx& c) const { return c.i; }
+    HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst& P) const {
+        const u64 v = shoup(src.x(c.s, j, d, P), c.w.x, c.w.y, P.q);
+        c.e[j] = v;
         return v;
     }
-    HS_DEV u64* scratch(int jb) const { return D + (size_t)jb * n; }
-    HS_DEV void store(int jb, u32 j, u64 v, const PrimeConst& P) const {
-        D[(size_t)jb * n + j] = shoup(v, P.n_inv, P.n_inv_sh, P.q);
+    HS_DEV u64* scratch(const Ctx& c) const { return c.dd; }
+    HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst& P) const {
+        c.dd[j] = shoup(v, P.n_inv, P.n_inv_sh, P.q);
     }
 };
 
@@ -167,30 +206,23 @@ struct JobModUp {                           // forward NTT, job = (b*(l+1)+i)*(l
     int l, L;
     u32 n;
     const PrimeConst* pc;
-    HS_DEV void decode(int jb, int& bi, int& i, int& m) const {
-        int t = jb % (l + 1);
-        bi = jb / (l + 1);
-        i = bi % (l + 1);
-        m = t < i ? t : t + 1;              // m in [0, l+1] \ {i}; l+1 = aux
+    struct Ctx {
+        const u64* d;        // digit i (coefficient domain, mod q_i)
+        u64* e;              // E[b][i][m]
+        u64 qsrc;
+        int pm;
+    };
+    HS_DEV Ctx make(int jb) const {
+        const int t = jb % (l + 1);
+        const int bi = jb / (l + 1);
+        const int i = bi % (l + 1);
+        const int m = t < i ? t : t + 1;     // m in [0, l+1] \ {i}; l+1 = aux
+        return Ctx{D + (size_t)bi * n, E + ((size_t)bi * (l + 2) + m) * n, pc[i].q, m <= l ? m : L + 1};
     }
-    HS_DEV int prime(int jb) const {
-        int bi, i, m;
-        decode(jb, bi, i, m);
-        return m <= l ? m : L + 1;
-    }
-    HS_DEV u64 load(int jb, u32 j, const PrimeConst& P) const {
-        int bi, i, m;
-        decode(jb, bi, i, m);
-        return lift_mod(D[(size_t)bi * n + j], pc[i].q, P);
-    }
-    HS_DEV u64* scratch(int jb) const {
-        int bi, i, m;
-        decode(jb, bi, i, m);
-        return E + ((size_t)bi * (l + 2) + m) * n;
-    }
-    HS_DEV void store(int jb, u32 j, u64 v, const PrimeConst& P) const {
-        scratch(jb)[j] = canon4(v, P);
-    }
+    HS_DEV int prime(const Ctx& c) const { return c.pm; }
+    HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst& P) const { return lift_mod(c.d[j], c.qsrc, P); }
+    HS_DEV u64* scratch(const Ctx& c) const { return c.e; }
+    HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst& P) const { c.e[j] = canon4(v, P); }
 };
 
 // Key inner product: ACC[b][c][m] = sum_i E[b][i][m][perm(k)] * K_b[c][i][m].
@@ -225,37 +257,55 @@ ks_inner_kernel(Dev d, int l, const u64* __restrict__ E, size_t e_item_stride,
     out[((size_t)(l + 2) + m) * n + k] = redc128(la, ha, P);
 }
 
-// ModDown addends (what is added to the key-switch output).
+// ModDown addends (what is added to the key-switch output), bound per CTA.
 struct AddNone {
-    HS_DEV u64 v(int, int, int, int, u32, const Dev&, const PrimeConst&) const { return 0; }
+    struct B {};
+    HS_DEV B bind(int, int, int, int, const Dev&) const { return B{}; }
+    HS_DEV u64 v(const B&, u32, const Dev&, const PrimeConst&) const { return 0; }
 };
 struct AddTensor {     // relinearize after mult_ct: d0 = a0 b0, d1 = a0 b1 + a1 b0
     ItemPtr a, bb;
-    HS_DEV u64 v(int b, int poly, int m, int l, u32 j, const Dev& d, const PrimeConst& P) const {
-        const size_t n = d.n;
+    struct B {
+        const u64 *a0, *a1, *b0, *b1;
+        int poly;
+    };
+    HS_DEV B bind(int b, int poly, int m, int l, const Dev& d) const {
         const u64* A = a.at(b);
-        const u64* B = bb.at(b);
-        const u64 a0 = A[m * n + j], b0 = B[m * n + j];
-        if (poly == 0) return mul_mod(a0, b0, P);
-        const u64 a1 = A[((size_t)(l + 1) + m) * n + j], b1 = B[((size_t)(l + 1) + m) * n + j];
+        const u64* Bp = bb.at(b);
+        const size_t o0 = (size_t)m * d.n, o1 = ((size_t)(l + 1) + m) * d.n;
+        return B{A + o0, A + o1, Bp + o0, Bp + o1, poly};
+    }
+    HS_DEV u64 v(const B& s, u32 j, const Dev&, const PrimeConst& P) const {
+        const u64 a0 = s.a0[j], b0 = s.b0[j];
+        if (s.poly == 0) return mul_mod(a0, b0, P);
         u64 lo = 0, hi = 0;
-        mac128(lo, hi, a0, b1);
-        mac128(lo, hi, a1, b0);
+        mac128(lo, hi, a0, s.b1[j]);
+        mac128(lo, hi, s.a1[j], b0);
         return barrett128(lo, hi, P);
     }
 };
 struct AddPoly {       // d0/d1 taken from a stored ct (npoly polys at level l)
     ItemPtr ct;
-    HS_DEV u64 v(int b, int poly, int m, int l, u32 j, const Dev& d, const PrimeConst&) const {
-        return ct.at(b)[((size_t)poly * (l + 1) + m) * d.n + j];
+    struct B {
+        const u64* p;
+    };
+    HS_DEV B bind(int b, int poly, int m, int l, const Dev& d) const {
+        return B{ct.at(b) + ((size_t)poly * (l + 1) + m) * d.n};
     }
+    HS_DEV u64 v(const B& s, u32 j, const Dev&, const PrimeConst&) const { return s.p[j]; }
 };
 struct AddPermC0 {     // rotation: automorphism_g(c0) on poly 0
     ItemPtr ct;
     const u32* gal;
-    HS_DEV u64 v(int b, int poly, int m, int l, u32 j, const Dev& d, const PrimeConst&) const {
-        if (poly) return 0;
-        return ct.at(b)[(size_t)m * d.n + galois_perm(j, gal[b], d.log_n)];
+    struct B {
+        const u64* c0;
+        u32 g;
+    };
+    HS_DEV B bind(int b, int poly, int m, int l, const Dev& d) const {
+        return B{poly ? nullptr : ct.at(b) + (size_t)m * d.n, poly ? 0u : gal[b]};
+    }
+    HS_DEV u64 v(const B& s, u32 j, const Dev& d, const PrimeConst&) const {
+        return s.c0 ? s.c0[galois_perm(j, s.g, d.log_n)] : 0ull;
     }
 };
 
@@ -267,21 +317,26 @@ struct JobModDown {                          // forward NTT, job = (b*2+c)*(l+1)
     Add add;
     int l;
     Dev d;
-    HS_DEV int prime(int jb) const { return jb % (l + 1); }
-    HS_DEV u64 load(int jb, u32 j, const PrimeConst& P) const {
-        return lift_mod(T[(size_t)(jb / (l + 1)) * d.n + j], d.aux_q, P);
+    struct Ctx {
+        const u64* t;        // INTT of the aux accumulator (coefficients mod p)
+        const u64* acc;      // ACC[b][c][m]
+        u64* out;            // out(b)[c][m]
+        typename Add::B add;
+        ulonglong2 w;        // p^-1 mod q_m
+        int m;
+    };
+    HS_DEV Ctx make(int jb) const {
+        const int bc = jb / (l + 1), m = jb % (l + 1);
+        const int b = bc >> 1, c = bc & 1;
+        return Ctx{T + (size_t)bc * d.n, ACC + ((size_t)bc * (l + 2) + m) * d.n,
+                   out.atw(b) + ((size_t)c * (l + 1) + m) * d.n, add.bind(b, c, m, l, d), d.auxinv[m], m};
     }
-    HS_DEV u64* scratch(int jb) const {
-        int bc = jb / (l + 1), m = jb % (l + 1);
-        return out.atw(bc >> 1) + ((size_t)(bc & 1) * (l + 1) + m) * d.n;
-    }
-    HS_DEV void store(int jb, u32 j, u64 v, const PrimeConst& P) const {
-        int bc = jb / (l + 1), m = jb % (l + 1);
-        u64 acc = ACC[((size_t)bc * (l + 2) + m) * d.n + j];
-        ulonglong2 w = d.auxinv[m];
-        u64 r = shoup(sub_mod(acc, canon4(v, P), P.q), w.x, w.y, P.q);
-        r = add_mod(r, add.v(bc >> 1, bc & 1, m, l, j, d, P), P.q);
-        scratch(jb)[j] = r;
+    HS_DEV int prime(const Ctx& c) const { return c.m; }
+    HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst& P) const { return lift_mod(c.t[j], d.aux_q, P); }
+    HS_DEV u64* scratch(const Ctx& c) const { return c.out; }
+    HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst& P) const {
+        u64 r = shoup(sub_mod(c.acc[j], canon4(v, P), P.q), c.w.x, c.w.y, P.q);
+        c.out[j] = add_mod(r, add.v(c.add, j, d, P), P.q);
     }
 };
 
@@ -341,7 +396,7 @@ modup_inner_kernel(Dev d, int l, const u64* __restrict__ E, const u64* const* __
 #pragma unroll
             for (int k = 0; k < NTT_EPT; k++) sm[spad(t + k * NTT_THREADS)] = src[t + k * NTT_THREADS];
             __syncthreads();
-            ntt_rounds_fwd<LB, H, 1, 0>(sm, tw, hi0, LA, P.q, P.two_q);
+            ntt_rounds_fwd<LB, H, 1>(sm, tw, hi0, LA, P.q, P.two_q);
 #pragma unroll
             for (int k = 0; k < NTT_EPT; k++) ext[k] = canon4(sm[spad(t + k * NTT_THREADS)], P);
             __syncthreads();
@@ -458,22 +513,30 @@ struct JobRescale {                          // forward NTT, job = (b*npoly+c)*l
     const PrimeConst* pc;
     const ulonglong2* qlinv;                 // row for level l
     u32 n;
-    HS_DEV int prime(int jb) const { return jb % l; }
-    HS_DEV u64 load(int jb, u32 j, const PrimeConst& P) const {
-        return lift_mod(T[(size_t)(jb / l) * n + j], pc[l].q, P);
+    struct Ctx {
+        const u64* t;        // INTT of the last limb (coefficients mod q_l)
+        const u64* x;        // in(b)[c][i]
+        u64* out;            // out(b)[c][i]
+        const u64* mask;     // mask(b)[i] (Montgomery form) or null
+        ulonglong2 w;        // q_l^-1 mod q_i
+        u64 ql;
+        int i;
+    };
+    HS_DEV Ctx make(int jb) const {
+        const int bc = jb / l, i = jb % l;
+        const int b = bc / npoly, c = bc % npoly;
+        const bool has_mask = mask.tab || mask.base;
+        return Ctx{T + (size_t)bc * n, in.at(b) + ((size_t)c * (l + 1) + i) * n,
+                   out.atw(b) + ((size_t)c * l + i) * n, has_mask ? mask.at(b) + (size_t)i * n : nullptr,
+                   qlinv[i], pc[l].q, i};
     }
-    HS_DEV u64* scratch(int jb) const {
-        int bc = jb / l, i = jb % l;
-        return out.atw(bc / npoly) + ((size_t)(bc % npoly) * l + i) * n;
-    }
-    HS_DEV void store(int jb, u32 j, u64 v, const PrimeConst& P) const {
-        int bc = jb / l, i = jb % l;
-        int b = bc / npoly, c = bc % npoly;
-        u64 x = in.at(b)[((size_t)c * (l + 1) + i) * n + j];
-        ulonglong2 w = qlinv[i];
-        u64 r = shoup(sub_mod(x, canon4(v, P), P.q), w.x, w.y, P.q);
-        if (mask.tab || mask.base) r = mont_mul(r, mask.at(b)[(size_t)i * n + j], P.q, P.qinv_neg);
-        scratch(jb)[j] = r;
+    HS_DEV int prime(const Ctx& c) const { return c.i; }
+    HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst& P) const { return lift_mod(c.t[j], c.ql, P); }
+    HS_DEV u64* scratch(const Ctx& c) const { return c.out; }
+    HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst& P) const {
+        u64 r = shoup(sub_mod(c.x[j], canon4(v, P), P.q), c.w.x, c.w.y, P.q);
+        if (c.mask) r = mont_mul(r, c.mask[j], P.q, P.qinv_neg);
+        c.out[j] = r;
     }
 };
 

@@ -98,3 +98,31 @@ def test_lazy_keys_inside_runner_match_resident_keys(pkg):
             assert lib().hs_keys_generated(ctx.handle) >= len(keys.galois)
             assert lib().hs_key_count(ctx.handle) == 1     # only the relin key stays resident
     assert np.array_equal(res[False], res["lazy"])
+
+
+def test_runner_n65536_lazy_keys_matches_oracle(pkg, oracle_mod):
+    """N = 2^16 (the north-star ring degree), L = 3, keys generated on demand."""
+    from paper_2604_11659_b200 import encmat, engine, formats
+    O = oracle_mod
+    n, sb, L, seed, dim = 1 << 16, 50, 3, 2024, 6
+    params = pkg.build_params(n, sb, L, seed)
+    ctx = pkg.CkksContext(params)
+    keys = ctx.keygen()
+    a = formats.generate_random_sparse(dim, 0.6, (17, 0))
+    b = formats.generate_random_sparse(dim, 0.6, (17, 1))
+    ea = encmat.encrypt_sparse(a, encmat.Layout.CSR, ctx, keys)
+    eb = encmat.encrypt_sparse(b, encmat.Layout.CSC, ctx, keys)
+    steps = encmat.required_rotation_steps(ea.meta, eb.meta)
+    keys = ctx.gen_galois_keys(steps, keys, device="lazy")
+    pairs = encmat.pair_array(ea.meta, eb.meta)
+    mc = engine.MaskCache(ctx, dim)
+    mc.prewarm(np.unique(np.minimum(pairs[:, 2], pairs[:, 3])))
+    res = engine.spmm_csr_csc(ea, eb, ctx, keys, engine.OpCounter(), mc)
+    octx = O.OracleContext(O.build_params(n, sb, L, seed))
+    okeys = octx.keygen()
+    octx.gen_galois_keys(O.rotation_steps(pairs.tolist(), dim), okeys)
+    masks = {int(p): np.stack(mc.get(int(p)).limbs) for p in np.unique(np.minimum(pairs[:, 2], pairs[:, 3]))}
+    want = octx.spmspm(ea.ctxt.host(), eb.ctxt.host(), pairs, dim, masks, okeys)
+    assert np.array_equal(res.ctxt.host(), want)
+    err = O.frobenius_error(encmat.decrypt_result(res, ctx, keys), O.plain_matmul(a, b))
+    assert err < 1e-6, err
