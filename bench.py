@@ -199,7 +199,8 @@ def roofline_probe(pkg, ctx, params, peaks):
     from paper_2604_11659_b200 import device as D
     from paper_2604_11659_b200._lib import check, lib
     n, L = params.ring_degree, params.levels
-    items = 512
+    # ModUp limb count of a pair batch, capped at ~2 GiB of limbs
+    items = max(1, min(512, (2 << 30) // (8 * n * (L + 1) * (L + 2))))
     limbs = items * (L + 1) * (L + 2)
     buf = D.zeros((limbs, n))
     st = torch.cuda.current_stream()

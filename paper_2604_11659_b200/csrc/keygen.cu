@@ -26,7 +26,10 @@
 
 namespace hs {
 
-constexpr int RNG_T = 1024;             // threads per key CTA = positions per chunk
+constexpr int RNG_T = 512;              // threads per key CTA
+constexpr int RNG_E = 8;                // draws per thread per chunk (positions t + k*RNG_T)
+constexpr int RNG_CH = RNG_T * RNG_E;   // positions per chunk
+constexpr int RNG_W = RNG_T / 32;       // warps
 
 struct U128 {
     u64 hi, lo;
@@ -56,9 +59,9 @@ struct ZigTables {
     u64 ki[256];
 };
 
-struct RngJump {                          // for t = 0..RNG_T: A_t = M^t, S_t = sum_{k<t} M^k
-    U128 A[RNG_T + 1];
-    U128 S[RNG_T + 1];
+struct RngJump {                          // for t = 0..RNG_CH: A_t = M^t, S_t = sum_{k<t} M^k
+    U128 A[RNG_CH + 1];
+    U128 S[RNG_CH + 1];
 };
 
 struct KeyStream {
@@ -93,64 +96,81 @@ constexpr double ZIG_INV_R = 0.27366123732975828;
 
 HS_DEV double next_double_of(u64 raw) { return (double)(raw >> 11) * (1.0 / 9007199254740992.0); }
 
-// Block-wide exclusive scan of a 0/1 flag (1024 threads); returns the prefix,
-// writes the block total to *total.
-HS_DEV u32 block_scan(u32 flag, u32* warp_sums, u32* total) {
-    const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const unsigned mask = __ballot_sync(0xffffffffu, flag);
-    const u32 pre = __popc(mask & ((1u << lane) - 1u));
-    if (lane == 0) warp_sums[warp] = __popc(mask);
+// Exclusive scan of the per-(k, warp) ballot counts of a chunk in stream
+// order (k-major, then warp, then lane).  cnt[] in/out; returns the total.
+HS_DEV u32 chunk_scan(u32* cnt, u32* s_total) {
     __syncthreads();
-    if (warp == 0) {
-        u32 v = warp_sums[lane];
-        u32 inc = v;
+    if (threadIdx.x < 32) {
+        const u32 lane = threadIdx.x;
+        constexpr int PER = RNG_E * RNG_W / 32;    // entries per lane
+        u32 v[PER > 0 ? PER : 1];
+        u32 sum = 0;
+#pragma unroll
+        for (int k = 0; k < PER; k++) {
+            v[k] = cnt[lane * PER + k];
+            sum += v[k];
+        }
+        u32 inc = sum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            u32 t = __shfl_up_sync(0xffffffffu, inc, o);
+            const u32 t = __shfl_up_sync(0xffffffffu, inc, o);
             if (lane >= (u32)o) inc += t;
         }
-        warp_sums[lane] = inc - v;
-        if (lane == 31) *total = inc;
+        u32 run = inc - sum;
+#pragma unroll
+        for (int k = 0; k < PER; k++) {
+            cnt[lane * PER + k] = run;
+            run += v[k];
+        }
+        if (lane == 31) *s_total = inc;
     }
     __syncthreads();
-    const u32 r = warp_sums[warp] + pre;
-    __syncthreads();
-    return r;
+    return *s_total;
 }
 
+// One CTA per key; thread t owns chunk positions t + k*RNG_T (k < RNG_E), so
+// shared-memory traffic is conflict free and stream order is k-major.
 __global__ void __launch_bounds__(RNG_T) keygen_stream_kernel(KeygenArgs A) {
-    __shared__ u64 raw[2][RNG_T];
-    __shared__ double xval[RNG_T];
-    __shared__ unsigned fastbits[RNG_T / 32];
-    __shared__ unsigned emitbits[RNG_T / 32];
-    __shared__ u32 warp_sums[32];
+    extern __shared__ u64 dyn[];
+    u64* raw0 = dyn;                                   // [2][RNG_CH] ring
+    double* xval = (double*)(dyn + 2 * RNG_CH);        // [RNG_CH]
+    __shared__ unsigned fastbits[RNG_CH / 32];
+    __shared__ unsigned emitbits[RNG_CH / 32];
+    __shared__ u32 cnt[RNG_E * RNG_W];
     __shared__ u32 s_total;
     __shared__ long long s_cursor;        // absolute stream position of the consumer
     __shared__ u32 s_count;               // outputs produced in the current segment
     __shared__ int s_seg;                 // segment index over the whole key
-    __shared__ u32 s_end;                 // chunk-relative end position of a finished segment
+    __shared__ u32 s_end;
 
-    const int k = blockIdx.x;
-    const u32 t = threadIdx.x;
+    const int key = blockIdx.x;
+    const u32 t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const unsigned lt = (1u << lane) - 1u;
     const int L = A.L;
     const u32 n = A.n;
     const int segs_per_digit = L + 3;     // (L+2) uniform + 1 normal
     const int nseg = (L + 1) * segs_per_digit;
-    const KeyStream ks = A.streams[k];
+    const KeyStream ks = A.streams[key];
     const U128 inc{ks.inc_hi, ks.inc_lo};
-    const U128 AT = A.jump->A[RNG_T];
-    const U128 CT = mul128(A.jump->S[RNG_T], inc);
-    // thread t holds the state whose output is position (chunk_base + t)
+    const U128 AT = A.jump->A[RNG_T], CT = mul128(A.jump->S[RNG_T], inc);       // stride within chunk
+    const U128 ACH = A.jump->A[RNG_CH], CCH = mul128(A.jump->S[RNG_CH], inc);  // chunk to chunk
+    // state whose output is position t of the next chunk to generate
     U128 st = add128(mul128(A.jump->A[t + 1], U128{ks.state_hi, ks.state_lo}),
                      mul128(A.jump->S[t + 1], inc));
-    u64* a_key = A.a_out[k];
-    long long* e_key = A.e_out + (size_t)k * (L + 1) * n;
+    u64* a_key = A.a_out[key];
+    long long* e_key = A.e_out + (size_t)key * (L + 1) * n;
 
-    // prime chunk 0 and chunk 1
-    raw[0][t] = xsl_rr(st);
-    st = add128(mul128(st, AT), CT);
-    raw[1][t] = xsl_rr(st);
-    st = add128(mul128(st, AT), CT);
+    auto generate = [&](u64* buf) {
+        U128 s = st;
+#pragma unroll
+        for (int k = 0; k < RNG_E; k++) {
+            buf[k * RNG_T + t] = xsl_rr(s);
+            s = add128(mul128(s, AT), CT);
+        }
+        st = add128(mul128(st, ACH), CCH);
+    };
+    generate(raw0);
+    generate(raw0 + RNG_CH);
     if (t == 0) {
         s_cursor = 0;
         s_count = 0;
@@ -161,68 +181,86 @@ __global__ void __launch_bounds__(RNG_T) keygen_stream_kernel(KeygenArgs A) {
     long long chunk_base = 0;
     int cur = 0;
     while (true) {
-        // consume the current chunk [chunk_base, chunk_base + RNG_T)
+        u64* raw = raw0 + cur * RNG_CH;
+        u64* nxt = raw0 + (cur ^ 1) * RNG_CH;
         while (true) {
             const int seg = s_seg;
             if (seg >= nseg) break;
             const long long cursor = s_cursor;
-            if (cursor >= chunk_base + RNG_T) break;
+            if (cursor >= chunk_base + RNG_CH) break;
             const int digit = seg / segs_per_digit;
             const int sidx = seg % segs_per_digit;
             const u32 count0 = s_count;
-            const long long p = chunk_base + t;
             if (sidx < L + 2) {
-                // ---- uniform segment: integers(0, q, n) by Lemire's method
-                const PrimeConst P = A.pc[sidx];
-                const u64 q = P.q;
+                // ---- uniform: integers(0, q, n), Lemire (accept iff lo >= (2^64-q) mod q)
+                const u64 q = A.pc[sidx].q;
                 const u64 thr = A.thr[sidx];
-                const u64 x = raw[cur][t];
-                const u64 lo = x * q, hi = __umul64hi(x, q);
-                const u32 acc = (p >= cursor && lo >= thr) ? 1u : 0u;
-                const u32 rank = block_scan(acc, warp_sums, &s_total);
-                const u32 idx = count0 + rank;
-                if (acc && idx < n) a_key[((size_t)digit * (L + 2) + sidx) * n + idx] = hi;
-                if (acc && idx == n - 1) s_end = t + 1;
+                u64 val[RNG_E];
+                unsigned ball[RNG_E];
+#pragma unroll
+                for (int k = 0; k < RNG_E; k++) {
+                    const u32 i = k * RNG_T + t;
+                    const u64 x = raw[i];
+                    const bool acc = chunk_base + i >= cursor && x * q >= thr;
+                    val[k] = __umul64hi(x, q);
+                    ball[k] = __ballot_sync(0xffffffffu, acc);
+                    if (lane == 0) cnt[k * RNG_W + warp] = __popc(ball[k]);
+                }
+                const u32 total = chunk_scan(cnt, &s_total);
+                u64* dst = a_key + ((size_t)digit * (L + 2) + sidx) * n;
+#pragma unroll
+                for (int k = 0; k < RNG_E; k++) {
+                    if (!((ball[k] >> lane) & 1u)) continue;
+                    const u32 idx = count0 + cnt[k * RNG_W + warp] + __popc(ball[k] & lt);
+                    if (idx < n) dst[idx] = val[k];
+                    if (idx == n - 1) s_end = k * RNG_T + t + 1;
+                }
                 __syncthreads();
                 if (t == 0) {
-                    if (count0 + s_total >= n) {
+                    if (count0 + total >= n) {
                         s_cursor = chunk_base + s_end;
                         s_count = 0;
                         s_seg = seg + 1;
                     } else {
-                        s_cursor = chunk_base + RNG_T;
-                        s_count = count0 + s_total;
+                        s_cursor = chunk_base + RNG_CH;
+                        s_count = count0 + total;
                     }
                 }
                 __syncthreads();
             } else {
-                // ---- normal segment: 0 + 3.2 * standard_normal, rint -> int64
-                const u64 r = raw[cur][t];
-                const int zi = (int)(r & 0xff);
-                const u64 r8 = r >> 8;
-                const u64 rabs = (r8 >> 1) & 0x000fffffffffffffull;
-                double x = (double)rabs * A.zig->wi[zi];
-                if (r8 & 1) x = -x;
-                const bool fast = rabs < A.zig->ki[zi];
-                xval[t] = x;
-                const unsigned fb = __ballot_sync(0xffffffffu, fast);
-                if ((t & 31) == 0) {
-                    fastbits[t >> 5] = fb;
-                    emitbits[t >> 5] = 0u;
+                // ---- normal: 0 + 3.2 * standard_normal (ziggurat), rint -> int64
+#pragma unroll
+                for (int k = 0; k < RNG_E; k++) {
+                    const u32 i = k * RNG_T + t;
+                    const u64 r = raw[i];
+                    const int zi = (int)(r & 0xff);
+                    const u64 r8 = r >> 8;
+                    const u64 rabs = (r8 >> 1) & 0x000fffffffffffffull;
+                    double x = (double)rabs * A.zig->wi[zi];
+                    if (r8 & 1) x = -x;
+                    xval[i] = x;
+                    const unsigned fb = __ballot_sync(0xffffffffu, rabs < A.zig->ki[zi]);
+                    if (lane == 0) {
+                        fastbits[i >> 5] = fb;
+                        emitbits[i >> 5] = 0u;
+                    }
                 }
                 __syncthreads();
                 if (t == 0) {
                     // token walk over [cursor, chunk end): fast tokens are 1 draw;
-                    // slow tokens need the following draw(s) (possibly next chunk)
+                    // slow tokens consume the following draw(s), maybe from the next chunk
                     long long c = cursor;
-                    u32 cnt = count0;
-                    const long long cend = chunk_base + RNG_T;
+                    u32 cntv = count0;
+                    const long long cend = chunk_base + RNG_CH;
                     bool done = false;
+                    auto draw_at = [&](long long pos) -> u64 {
+                        const long long rp = pos - chunk_base;
+                        return rp < RNG_CH ? raw[rp] : nxt[rp - RNG_CH];
+                    };
                     while (c < cend && !done) {
-                        u32 rel = (u32)(c - chunk_base);
-                        // next non-fast position at or after rel
-                        u32 s = RNG_T;
-                        for (u32 w = rel >> 5; w < RNG_T / 32; w++) {
+                        const u32 rel = (u32)(c - chunk_base);
+                        u32 s = RNG_CH;
+                        for (u32 w = rel >> 5; w < RNG_CH / 32; w++) {
                             unsigned bits = ~fastbits[w];
                             if (w == (rel >> 5)) bits &= ~((1u << (rel & 31)) - 1u);
                             if (bits) {
@@ -231,32 +269,23 @@ __global__ void __launch_bounds__(RNG_T) keygen_stream_kernel(KeygenArgs A) {
                             }
                         }
                         u32 run = s - rel;
-                        if (cnt + run >= n) {
-                            run = n - cnt;
+                        if (cntv + run >= n) {
+                            run = n - cntv;
                             done = true;
                         }
                         set_bit_range(emitbits, rel, rel + run);
-                        cnt += run;
+                        cntv += run;
                         c += run;
-                        if (done || s >= RNG_T) break;
-                        // slow token at chunk position s (c == chunk_base + s)
-                        const u64 rs = raw[cur][s];
+                        if (done || s >= RNG_CH) break;
+                        const u64 rs = raw[s];
                         const int zs = (int)(rs & 0xff);
                         const u64 rabs_s = ((rs >> 8) >> 1) & 0x000fffffffffffffull;
-                        // draw following position c: in this chunk or the next one
-                        auto draw_at = [&](long long pos) -> u64 {
-                            const long long rp = pos - chunk_base;
-                            return rp < RNG_T ? raw[cur][rp] : raw[cur ^ 1][rp - RNG_T];
-                        };
                         if (zs != 0) {
                             const double xs = xval[s];
                             const double u = next_double_of(draw_at(c + 1));
-                            const bool ok = (A.zig->fi[zs - 1] - A.zig->fi[zs]) * u + A.zig->fi[zs] <
-                                            exp(-0.5 * xs * xs);
-                            if (ok) {
+                            if ((A.zig->fi[zs - 1] - A.zig->fi[zs]) * u + A.zig->fi[zs] < exp(-0.5 * xs * xs)) {
                                 emitbits[s >> 5] |= 1u << (s & 31);
-                                cnt++;
-                                if (cnt >= n) done = true;
+                                if (++cntv >= n) done = true;
                             }
                             c += 2;
                         } else {
@@ -273,40 +302,48 @@ __global__ void __launch_bounds__(RNG_T) keygen_stream_kernel(KeygenArgs A) {
                             }
                             xval[s] = v;
                             emitbits[s >> 5] |= 1u << (s & 31);
-                            cnt++;
-                            if (cnt >= n) done = true;
+                            if (++cntv >= n) done = true;
                             c = pos;
                         }
                     }
-                    // done: the segment's end is c (absolute)
                     s_cursor = c;
-                    s_count = done ? n : cnt;
                     s_end = done ? 1u : 0u;
                 }
                 __syncthreads();
-                const u32 em = (emitbits[t >> 5] >> (t & 31)) & 1u;
-                const u32 rank = block_scan(em, warp_sums, &s_total);
-                if (em) {
-                    const double v = 0.0 + 3.2 * xval[t];
-                    e_key[(size_t)digit * n + count0 + rank] = (long long)rint(v);
+                unsigned ball[RNG_E];
+#pragma unroll
+                for (int k = 0; k < RNG_E; k++) {
+                    const u32 i = k * RNG_T + t;
+                    ball[k] = __ballot_sync(0xffffffffu, (emitbits[i >> 5] >> (i & 31)) & 1u);
+                    if (lane == 0) cnt[k * RNG_W + warp] = __popc(ball[k]);
+                }
+                chunk_scan(cnt, &s_total);
+                long long* dst = e_key + (size_t)digit * n;
+#pragma unroll
+                for (int k = 0; k < RNG_E; k++) {
+                    if (!((ball[k] >> lane) & 1u)) continue;
+                    const u32 i = k * RNG_T + t;
+                    const u32 idx = count0 + cnt[k * RNG_W + warp] + __popc(ball[k] & lt);
+                    dst[idx] = (long long)rint(0.0 + 3.2 * xval[i]);
                 }
                 __syncthreads();
                 if (t == 0) {
                     if (s_end) {
                         s_count = 0;
                         s_seg = seg + 1;
+                    } else {
+                        s_count = count0 + s_total;
                     }
                 }
                 __syncthreads();
             }
         }
         if (s_seg >= nseg) break;
-        // advance the ring: chunk c+1 becomes current, generate chunk c+2
+        // ring advance: chunk c+1 becomes current, generate chunk c+2 in place of c
         __syncthreads();
-        raw[cur][t] = xsl_rr(st);
-        st = add128(mul128(st, AT), CT);
+        generate(raw);
         cur ^= 1;
-        chunk_base += RNG_T;
+        chunk_base += RNG_CH;
         __syncthreads();
     }
 }
@@ -341,7 +378,13 @@ void keygen_streams(const Dev& d, int K, const void* streams, u64* const* a_out,
                     const void* jump, const void* zig, const u64* thr, cudaStream_t st) {
     KeygenArgs A{(const KeyStream*)streams, a_out, e_out, (const RngJump*)jump, (const ZigTables*)zig,
                  d.pc, thr, d.L, d.n};
-    keygen_stream_kernel<<<K, RNG_T, 0, st>>>(A);
+    constexpr size_t smem = (size_t)3 * RNG_CH * sizeof(u64);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(keygen_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    keygen_stream_kernel<<<K, RNG_T, smem, st>>>(A);
     note_launch();
 }
 
@@ -400,15 +443,63 @@ struct JobKeyB {
     }
 };
 
+// Fully fused key assembly: one forward NTT per (key, digit i, modulus m)
+// whose loader reduces e_i mod q_m and whose epilogue forms
+//   b = NTT(e_i) + [m<=L] f_im sk(X^g)_m - a_im sk_m
+// and writes both b and a in Montgomery form (the device key layout).
+struct JobKeyFused {
+    u64* const* keys;
+    const long long* e;          // [K][L+1][n]
+    const u32* gal;
+    const u64* sk;               // [L+2][n]
+    const ulonglong2* f;         // [(L+1)^2]
+    int per, L;
+    Dev d;
+    struct Ctx {
+        u64* b;
+        u64* a;
+        const long long* e;
+        const u64* skm;
+        ulonglong2 f;
+        u32 g;
+        int m;
+    };
+    HS_DEV Ctx make(int jb) const {
+        const int kk = jb / per, limb = jb % per;
+        const int i = limb / (L + 2), m = limb % (L + 2);
+        u64* key = keys[kk];
+        const size_t half = (size_t)per * d.n;
+        return Ctx{key + (size_t)limb * d.n, key + half + (size_t)limb * d.n,
+                   e + ((size_t)kk * (L + 1) + i) * d.n, sk + (size_t)m * d.n,
+                   m <= L ? f[i * (L + 1) + m] : make_ulonglong2(0, 0), gal[kk], m};
+    }
+    HS_DEV int prime(const Ctx& c) const { return c.m; }
+    HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst& P) const {
+        const long long v = c.e[j];
+        if (v >= 0) return reduce64((u64)v, P);
+        const u64 t = reduce64((u64)(-(v + 1)) + 1ull, P);
+        return t ? P.q - t : 0ull;
+    }
+    HS_DEV u64* scratch(const Ctx& c) const { return c.b; }
+    HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst& P) const {
+        u64 acc = csub(csub(v, P.two_q), P.q);
+        if (c.m <= L) {
+            const u32 br = __brev(j) >> (32 - d.log_n);
+            const u32 ex = (u32)((((u64)(2 * br + 1)) * c.g) & ((2ull << d.log_n) - 1));
+            const u32 pj = __brev((ex - 1) >> 1) >> (32 - d.log_n);
+            acc = add_mod(acc, shoup(c.skm[pj], c.f.x, c.f.y, P.q), P.q);
+        }
+        const u64 a = c.a[j];
+        acc = sub_mod(acc, mul_mod(a, c.skm[j], P), P.q);
+        c.b[j] = mont_mul(acc, P.r2_mod, P.q, P.qinv_neg);
+        c.a[j] = mont_mul(a, P.r2_mod, P.q, P.qinv_neg);
+    }
+};
+
 void keygen_assemble(const Dev& d, int K, u64* const* keys, const long long* e, const u32* gal,
                      const u64* sk, const ulonglong2* f, cudaStream_t st) {
     const int per = (d.L + 1) * (d.L + 2);
-    e_to_limbs_kernel<<<dim3((d.n + 255) / 256, per, K), 256, 0, st>>>(d, e, keys);
-    note_launch();
-    launch_ntt<true>(d, JobKeyB{keys, per, d.L, d.n}, K * per, st);
-    ksk_galois_combine(d, K, keys, gal, sk, f, st);
-    mont_keys_kernel<<<dim3((d.n + 255) / 256, 2 * per, K), 256, 0, st>>>(d, keys);
-    note_launch();
+    launch_ntt<true>(d, JobKeyFused{keys, e, gal, sk, f, per, d.L, d}, K * per, st);
 }
 
 size_t rng_jump_bytes() { return sizeof(RngJump); }
@@ -430,7 +521,7 @@ hs_status ensure_keygen_tables(hs_ctx* c) {
     const int L = c->L;
     RngJump* J = new RngJump();
     u128h a = 1, s = 0;
-    for (int t = 0; t <= RNG_T; t++) {
+    for (int t = 0; t <= RNG_CH; t++) {
         J->A[t] = U128{(u64)(a >> 64), (u64)a};
         J->S[t] = U128{(u64)(s >> 64), (u64)s};
         s += a;

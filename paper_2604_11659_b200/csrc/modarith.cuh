@@ -84,3 +84,16 @@ HS_DEV u64 lift_mod(u64 v, u64 q_src, const PrimeConst& D) {
     u64 t = reduce64(neg ? q_src - v : v, D);
     return (neg && t) ? D.q - t : t;
 }
+
+// Same lift when the caller knows q_src/2 < q_dst (no reduction needed):
+// the magnitude of the centred value already is a residue mod q_dst.
+HS_DEV u64 lift_mod_small(u64 v, u64 q_src, u64 q_dst) {
+    const bool neg = v > (q_src >> 1);
+    const u64 t = neg ? q_src - v : v;
+    return (neg && t) ? q_dst - t : t;
+}
+
+// Dispatch on a CTA-uniform flag.
+HS_DEV u64 lift_mod_sel(u64 v, u64 q_src, const PrimeConst& D, bool small) {
+    return small ? lift_mod_small(v, q_src, D.q) : lift_mod(v, q_src, D);
+}

@@ -211,16 +211,21 @@ struct JobModUp {                           // forward NTT, job = (b*(l+1)+i)*(l
         u64* e;              // E[b][i][m]
         u64 qsrc;
         int pm;
+        bool small;          // q_i / 2 < q_m: the lift needs no reduction
     };
     HS_DEV Ctx make(int jb) const {
         const int t = jb % (l + 1);
         const int bi = jb / (l + 1);
         const int i = bi % (l + 1);
         const int m = t < i ? t : t + 1;     // m in [0, l+1] \ {i}; l+1 = aux
-        return Ctx{D + (size_t)bi * n, E + ((size_t)bi * (l + 2) + m) * n, pc[i].q, m <= l ? m : L + 1};
+        const int pm = m <= l ? m : L + 1;
+        const u64 qs = pc[i].q;
+        return Ctx{D + (size_t)bi * n, E + ((size_t)bi * (l + 2) + m) * n, qs, pm, (qs >> 1) < pc[pm].q};
     }
     HS_DEV int prime(const Ctx& c) const { return c.pm; }
-    HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst& P) const { return lift_mod(c.d[j], c.qsrc, P); }
+    HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst& P) const {
+        return lift_mod_sel(c.d[j], c.qsrc, P, c.small);
+    }
     HS_DEV u64* scratch(const Ctx& c) const { return c.e; }
     HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst& P) const { c.e[j] = canon4(v, P); }
 };
@@ -324,15 +329,19 @@ struct JobModDown {                          // forward NTT, job = (b*2+c)*(l+1)
         typename Add::B add;
         ulonglong2 w;        // p^-1 mod q_m
         int m;
+        bool small;          // p / 2 < q_m
     };
     HS_DEV Ctx make(int jb) const {
         const int bc = jb / (l + 1), m = jb % (l + 1);
         const int b = bc >> 1, c = bc & 1;
         return Ctx{T + (size_t)bc * d.n, ACC + ((size_t)bc * (l + 2) + m) * d.n,
-                   out.atw(b) + ((size_t)c * (l + 1) + m) * d.n, add.bind(b, c, m, l, d), d.auxinv[m], m};
+                   out.atw(b) + ((size_t)c * (l + 1) + m) * d.n, add.bind(b, c, m, l, d), d.auxinv[m], m,
+                   (d.aux_q >> 1) < d.pc[m].q};
     }
     HS_DEV int prime(const Ctx& c) const { return c.m; }
-    HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst& P) const { return lift_mod(c.t[j], d.aux_q, P); }
+    HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst& P) const {
+        return lift_mod_sel(c.t[j], d.aux_q, P, c.small);
+    }
     HS_DEV u64* scratch(const Ctx& c) const { return c.out; }
     HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst& P) const {
         u64 r = shoup(sub_mod(c.acc[j], canon4(v, P), P.q), c.w.x, c.w.y, P.q);
@@ -521,6 +530,7 @@ struct JobRescale {                          // forward NTT, job = (b*npoly+c)*l
         ulonglong2 w;        // q_l^-1 mod q_i
         u64 ql;
         int i;
+        bool small;          // q_l / 2 < q_i
     };
     HS_DEV Ctx make(int jb) const {
         const int bc = jb / l, i = jb % l;
@@ -528,10 +538,12 @@ struct JobRescale {                          // forward NTT, job = (b*npoly+c)*l
         const bool has_mask = mask.tab || mask.base;
         return Ctx{T + (size_t)bc * n, in.at(b) + ((size_t)c * (l + 1) + i) * n,
                    out.atw(b) + ((size_t)c * l + i) * n, has_mask ? mask.at(b) + (size_t)i * n : nullptr,
-                   qlinv[i], pc[l].q, i};
+                   qlinv[i], pc[l].q, i, (pc[l].q >> 1) < pc[i].q};
     }
     HS_DEV int prime(const Ctx& c) const { return c.i; }
-    HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst& P) const { return lift_mod(c.t[j], c.ql, P); }
+    HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst& P) const {
+        return lift_mod_sel(c.t[j], c.ql, P, c.small);
+    }
     HS_DEV u64* scratch(const Ctx& c) const { return c.out; }
     HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst& P) const {
         u64 r = shoup(sub_mod(c.x[j], canon4(v, P), P.q), c.w.x, c.w.y, P.q);
