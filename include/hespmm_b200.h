@@ -72,7 +72,7 @@ hs_status hs_ctx_tables(const hs_ctx* ctx, uint32_t p, uint64_t* roots, uint64_t
                         uint64_t* iroots, uint64_t* iroots_sh, uint64_t* n_inv, uint64_t* mu);
 
 /* ------------------------------------------------------------------- keys
- * Key switching keys live inside the context (device, Montgomery form).
+ * Key switching keys live inside the context (device, standard form).
  * kind 0 = relinearisation key (KeyBundle.relin), kind 1 = Galois key for
  * normalised step `step` in [1, slots) (KeyBundle.galois[step]). */
 hs_status hs_key_upload(hs_ctx* ctx, int kind, uint32_t step, const uint64_t* key, int key_on_host,

@@ -315,8 +315,6 @@ hs_status hs_key_upload(hs_ctx* c, int kind, uint32_t step, const uint64_t* key,
     }
     HS_CUDA(cudaMemcpyAsync(kb->d, key, c->key_bytes(),
                             on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, ST(stream)));
-    to_montgomery(c->dev, kb->d, (size_t)2 * (c->L + 1) * (c->L + 2),
-                  prime_map_range(0, c->L + 2), false, ST(stream));
     CHECK_LAUNCH();
     return (hs_status)HS_OK;
 }
@@ -354,7 +352,6 @@ hs_status hs_key_generate(hs_ctx* c, int kind, uint32_t step, const uint64_t* a,
     HS_CUDA(cudaMallocAsync((void**)&d_f, f.size() * sizeof(ulonglong2), st));
     HS_CUDA(cudaMemcpyAsync(d_f, f.data(), f.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice, st));
     ksk_combine(c->dev, kb->d, ntt_e, target, sk, d_f, st);
-    to_montgomery(c->dev, kb->d, (size_t)2 * (L + 1) * (L + 2), prime_map_range(0, L + 2), false, st);
     CHECK_LAUNCH();
     HS_CUDA(cudaStreamSynchronize(st));   // f is a stack vector
     cudaFreeAsync(ntt_e, st);
@@ -370,8 +367,6 @@ hs_status hs_key_download(hs_ctx* c, int kind, uint32_t step, uint64_t* out, voi
         return (hs_status)HS_KEY_MISSING;
     }
     HS_CUDA(cudaMemcpyAsync(out, kb->d, c->key_bytes(), cudaMemcpyDeviceToDevice, ST(stream)));
-    to_montgomery(c->dev, out, (size_t)2 * (c->L + 1) * (c->L + 2), prime_map_range(0, c->L + 2),
-                  true, ST(stream));
     CHECK_LAUNCH();
     return (hs_status)HS_OK;
 }

@@ -31,7 +31,7 @@ void set_error(const std::string& msg);
 void note_launch(int count = 1);
 
 struct KeyBuf {
-    u64* d = nullptr;            // [2][L+1][L+2][n], Montgomery form
+    u64* d = nullptr;            // [2][L+1][L+2][n], standard form
 };
 
 }  // namespace hs

@@ -446,7 +446,7 @@ struct JobKeyB {
 // Fully fused key assembly: one forward NTT per (key, digit i, modulus m)
 // whose loader reduces e_i mod q_m and whose epilogue forms
 //   b = NTT(e_i) + [m<=L] f_im sk(X^g)_m - a_im sk_m
-// and writes both b and a in Montgomery form (the device key layout).
+// (keys are kept in standard form; a is left as drawn).
 struct JobKeyFused {
     u64* const* keys;
     const long long* e;          // [K][L+1][n]
@@ -489,10 +489,7 @@ struct JobKeyFused {
             const u32 pj = __brev((ex - 1) >> 1) >> (32 - d.log_n);
             acc = add_mod(acc, shoup(c.skm[pj], c.f.x, c.f.y, P.q), P.q);
         }
-        const u64 a = c.a[j];
-        acc = sub_mod(acc, mul_mod(a, c.skm[j], P), P.q);
-        c.b[j] = mont_mul(acc, P.r2_mod, P.q, P.qinv_neg);
-        c.a[j] = mont_mul(a, P.r2_mod, P.q, P.qinv_neg);
+        c.b[j] = sub_mod(acc, mul_mod(c.a[j], c.skm[j], P), P.q);
     }
 };
 
@@ -613,7 +610,7 @@ hs_status generate_galois_keys(hs_ctx* c, const std::vector<u32>& steps,
                                 cudaMemcpyHostToDevice, st));
         keygen_streams(c->dev, K, d_streams, d_aout, e, c->d_jump, c->d_zig, c->d_thr, st);
         keygen_assemble(c->dev, K, d_keys, e, d_gal, c->d_sk, c->d_kskf, st);
-        HS_CUDA(cudaStreamSynchronize(st));   // host staging vectors are reused
+        // pageable host staging is copied at call time; device arrays are stream-ordered
         c->keys_generated += K;
     }
     cudaFreeAsync(e, st);

@@ -43,6 +43,13 @@ HS_DEV u64 redc128(u64 lo, u64 hi, const PrimeConst& P) {
     return csub(r, P.q);
 }
 
+// Key inner products: keys are kept in standard form, so the REDC result
+// X 2^-64 is brought back with one Montgomery product by 2^128 mod q --
+// one conversion per output instead of one per key element.
+HS_DEV u64 redc128_std(u64 lo, u64 hi, const PrimeConst& P) {
+    return mont_mul(redc128(lo, hi, P), P.r2_mod, P.q, P.qinv_neg);
+}
+
 // Barrett reduction of a 128-bit value x < 2 q^2 (same estimate as mul_mod).
 HS_DEV u64 barrett128(u64 lo, u64 hi, const PrimeConst& P) {
     u64 q1 = (hi << (65 - P.k)) | (lo >> (P.k - 1));
@@ -231,7 +238,7 @@ struct JobModUp {                           // forward NTT, job = (b*(l+1)+i)*(l
 };
 
 // Key inner product: ACC[b][c][m] = sum_i E[b][i][m][perm(k)] * K_b[c][i][m].
-// Keys are stored in Montgomery form, so one REDC of the 128-bit sum yields
+// Keys are stored in standard form; redc128_std turns the 128-bit sum into
 // the plain residue.  grid = (n/256, l+2, B).
 __global__ void __launch_bounds__(256)
 ks_inner_kernel(Dev d, int l, const u64* __restrict__ E, size_t e_item_stride,
@@ -258,8 +265,8 @@ ks_inner_kernel(Dev d, int l, const u64* __restrict__ E, size_t e_item_stride,
         mac128(la, ha, e, ka[(size_t)i * kstride]);
     }
     u64* out = ACC + (size_t)b * 2 * (l + 2) * n;
-    out[(size_t)m * n + k] = redc128(lb, hb, P);
-    out[((size_t)(l + 2) + m) * n + k] = redc128(la, ha, P);
+    out[(size_t)m * n + k] = redc128_std(lb, hb, P);
+    out[((size_t)(l + 2) + m) * n + k] = redc128_std(la, ha, P);
 }
 
 // ModDown addends (what is added to the key-switch output), bound per CTA.
@@ -421,8 +428,8 @@ modup_inner_kernel(Dev d, int l, const u64* __restrict__ E, const u64* const* __
     u64* out = ACC + (size_t)b * 2 * (l + 2) * n + j0;
 #pragma unroll
     for (int k = 0; k < NTT_EPT; k++) {
-        out[(size_t)m * n + t + k * NTT_THREADS] = redc128(lb[k], hb[k], P);
-        out[(size_t)(l + 2 + m) * n + t + k * NTT_THREADS] = redc128(la[k], ha[k], P);
+        out[(size_t)m * n + t + k * NTT_THREADS] = redc128_std(lb[k], hb[k], P);
+        out[(size_t)(l + 2 + m) * n + t + k * NTT_THREADS] = redc128_std(la[k], ha[k], P);
     }
 }
 

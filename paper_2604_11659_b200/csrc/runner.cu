@@ -99,29 +99,56 @@ struct DeviceArena {
 
 // Galois keys for a set of steps: resident keys from the context store, or
 // keys generated on the device on demand (steps registered with
-// hs_keygen_register), owned here and freed when no longer needed.
+// hs_keygen_register).  Generated keys live in a fixed pool of `cap` key
+// buffers; generation runs on a side stream so the next batch's keys are
+// produced while the current batch computes (events order reuse).
 struct KeyProvider {
     hs_ctx* c;
     cudaStream_t st;
-    std::unordered_map<u32, u64*> temp;
+    cudaStream_t side = nullptr;
+    std::vector<u64*> buf;
+    std::vector<int64_t> tag, last;
+    std::vector<cudaEvent_t> gen_ev, use_ev;
+    int64_t clock = 0;
+
     ~KeyProvider() {
-        for (auto& kv : temp) cudaFreeAsync(kv.second, st);
+        if (side) cudaStreamSynchronize(side);
+        cudaStreamSynchronize(st);
+        for (u64* b : buf) cudaFree(b);
+        for (auto e : gen_ev) cudaEventDestroy(e);
+        for (auto e : use_ev) cudaEventDestroy(e);
+        if (side) cudaStreamDestroy(side);
     }
-    bool needs_generation(u32 r) const { return !c->galois.count(r) && !temp.count(r); }
-    void release_except(const std::vector<u32>& keep) {
-        for (auto it = temp.begin(); it != temp.end();) {
-            if (std::find(keep.begin(), keep.end(), it->first) == keep.end()) {
-                cudaFreeAsync(it->second, st);
-                it = temp.erase(it);
-            } else {
-                ++it;
-            }
+    bool resident(u32 r) const { return c->galois.count(r) != 0; }
+    int slot_of(u32 r) const {
+        for (size_t k = 0; k < tag.size(); k++)
+            if (tag[k] == (int64_t)r) return (int)k;
+        return -1;
+    }
+    bool needs_generation(u32 r) const { return !resident(r) && slot_of(r) < 0; }
+    hs_status init(int cap) {
+        if (!buf.empty() || cap <= 0) return HS_OK;
+        HS_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+        buf.assign(cap, nullptr);
+        tag.assign(cap, -1);
+        last.assign(cap, 0);
+        gen_ev.resize(cap);
+        use_ev.resize(cap);
+        for (int k = 0; k < cap; k++) {
+            HS_CUDA(cudaMalloc((void**)&buf[k], c->key_bytes()));
+            HS_CUDA(cudaEventCreateWithFlags(&gen_ev[k], cudaEventDisableTiming));
+            HS_CUDA(cudaEventCreateWithFlags(&use_ev[k], cudaEventDisableTiming));
+            HS_CUDA(cudaEventRecord(use_ev[k], st));
         }
+        return HS_OK;
     }
-    hs_status get(const std::vector<u32>& steps, std::vector<const u64*>& out) {
+    // Start generating the missing keys of `steps` on the side stream, never
+    // evicting keys of `protect`.
+    hs_status prefetch(const std::vector<u32>& steps, const std::vector<u32>& protect) {
         std::vector<u32> gen;
         std::vector<hs_ctx::Stream> ss;
         std::vector<u64*> dst;
+        std::vector<int> slots;
         for (u32 r : steps) {
             if (!needs_generation(r) || std::find(gen.begin(), gen.end(), r) != gen.end()) continue;
             auto lz = c->lazy.find(r);
@@ -129,24 +156,54 @@ struct KeyProvider {
                 set_error("missing Galois key for step " + std::to_string(r));
                 return HS_KEY_MISSING;
             }
-            u64* buf = nullptr;
-            if (cudaMallocAsync((void**)&buf, c->key_bytes(), st) != cudaSuccess) {
-                set_error("out of device memory for generated Galois keys");
+            int victim = -1;
+            for (int k = 0; k < (int)buf.size(); k++) {
+                const bool keep = tag[k] >= 0 &&
+                                  (std::find(protect.begin(), protect.end(), (u32)tag[k]) != protect.end() ||
+                                   std::find(steps.begin(), steps.end(), (u32)tag[k]) != steps.end());
+                if (keep || std::find(slots.begin(), slots.end(), k) != slots.end()) continue;
+                if (victim < 0 || tag[k] < 0 || (tag[victim] >= 0 && last[k] < last[victim])) victim = k;
+                if (tag[victim] < 0) break;
+            }
+            if (victim < 0) {
+                set_error("Galois key pool exhausted");
                 return HS_OUT_OF_MEMORY;
             }
-            temp[r] = buf;
+            HS_CUDA(cudaStreamWaitEvent(side, use_ev[victim], 0));
+            tag[victim] = r;
+            last[victim] = ++clock;
             gen.push_back(r);
             ss.push_back(lz->second);
-            dst.push_back(buf);
+            dst.push_back(buf[victim]);
+            slots.push_back(victim);
         }
-        if (!gen.empty()) {
-            hs_status s = generate_galois_keys(c, gen, ss, dst, st);
-            if (s != HS_OK) return s;
-        }
+        if (gen.empty()) return HS_OK;
+        hs_status s = generate_galois_keys(c, gen, ss, dst, side);
+        if (s != HS_OK) return s;
+        for (int k : slots) HS_CUDA(cudaEventRecord(gen_ev[k], side));
+        return HS_OK;
+    }
+    hs_status acquire(const std::vector<u32>& steps, std::vector<const u64*>& out) {
+        hs_status s = prefetch(steps, steps);
+        if (s != HS_OK) return s;
         out.resize(steps.size());
         for (size_t k = 0; k < steps.size(); k++) {
             auto it = c->galois.find(steps[k]);
-            out[k] = it != c->galois.end() ? it->second.d : temp[steps[k]];
+            if (it != c->galois.end()) {
+                out[k] = it->second.d;
+                continue;
+            }
+            const int sl = slot_of(steps[k]);
+            HS_CUDA(cudaStreamWaitEvent(st, gen_ev[sl], 0));
+            last[sl] = ++clock;
+            out[k] = buf[sl];
+        }
+        return HS_OK;
+    }
+    hs_status release(const std::vector<u32>& steps) {
+        for (u32 r : steps) {
+            const int sl = slot_of(r);
+            if (sl >= 0) HS_CUDA(cudaEventRecord(use_ev[sl], st));
         }
         return HS_OK;
     }
@@ -268,10 +325,19 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, cons
     }
 
     DeviceArena A{st};
-    KeyProvider KP{c, st, {}};
+    KeyProvider KP{c, st};
     const size_t budget = c->batch_bytes;
-    // generated keys per chunk/batch are bounded by twice the work budget
-    const int64_t max_gen = std::max<int64_t>(1, (int64_t)(2 * budget / c->key_bytes()));
+    // generated keys per chunk/batch: the key pool holds two such sets (the
+    // one in use and the one being prefetched), bounded by twice the budget
+    const int64_t max_gen = std::max<int64_t>(1, (int64_t)(budget / c->key_bytes()));
+    bool lazy_needed = false;
+    for (const auto& al : align_list) lazy_needed |= !c->galois.count(al.second);
+    for (int64_t t = lo; t < hi && !lazy_needed; t++)
+        lazy_needed |= accr[order[t]] && !c->galois.count(accr[order[t]]);
+    if (lazy_needed) {
+        hs_status ks_ = KP.init((int)(2 * max_gen));
+        if (ks_ != HS_OK) return ks_;
+    }
 
     // ---- phase 1: hoisted alignment rotations
     u64* aligned = A.get<u64>(need.size() * ctL);
@@ -298,7 +364,7 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, cons
         int64_t rmax = budget / 8 > base_e ? (int64_t)((budget / 8 - base_e) / per_e) : 1;
         rmax = std::max<int64_t>(1, std::min<int64_t>(rmax, R));
         bool any_gen = false;
-        for (u32 r : steps_src) any_gen |= KP.needs_generation(r);
+        for (u32 r : steps_src) any_gen |= !KP.resident(r);
         if (any_gen) rmax = std::min<int64_t>(rmax, max_gen);
         u64* scratch = A.get<u64>(ks_hoisted_scratch_elems((int)rmax, L, n));
         u32* d_gal = A.get<u32>(R);
@@ -315,12 +381,17 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, cons
             const int rc = std::min<int>((int)rmax, R - r0);
             std::vector<u32> chunk(steps_src.begin() + r0, steps_src.begin() + r0 + rc);
             std::vector<const u64*> kp;
-            KP.release_except(chunk);
-            hs_status ks_ = KP.get(chunk, kp);
+            hs_status ks_ = KP.acquire(chunk, kp);
             if (ks_ != HS_OK) return ks_;
+            if (any_gen && r0 + rc < R) {      // next chunk's keys while this one computes
+                const int rn = std::min<int>((int)rmax, R - r0 - rc);
+                ks_ = KP.prefetch(std::vector<u32>(steps_src.begin() + r0 + rc,
+                                                   steps_src.begin() + r0 + rc + rn), chunk);
+                if (ks_ != HS_OK) return ks_;
+            }
             HS_CUDA(cudaMemcpyAsync(d_keys + r0, kp.data(), rc * sizeof(u64*), cudaMemcpyHostToDevice, st));
             rotate_hoisted(d, rc, L, sp, d_gal + r0, d_keys + r0, table(d_outs + r0), scratch, st);
-            if (any_gen) HS_CUDA(cudaStreamSynchronize(st));   // kp staging
+            KP.release(chunk);
         }
     }
 
@@ -363,25 +434,38 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, cons
 
     std::vector<u32> hR(P);
     for (int64_t t = 0; t < P; t++) hR[t] = accr[order[lo + t]];
+    // batches: up to B pairs and at most max_gen distinct non-resident keys
+    std::vector<int64_t> bstart;
+    std::vector<std::vector<u32>> bsteps_all;
     for (int64_t s = 0, bnext; s < P; s = bnext) {
-        // batch: up to B pairs, and at most max_gen distinct keys still to generate
         std::vector<u32> bsteps;
         int64_t ngen = 0;
         bnext = s;
         while (bnext < P && bnext - s < B) {
             const u32 r = hR[bnext];
             if (r && (bsteps.empty() || bsteps.back() != r)) {
-                if (KP.needs_generation(r) && ngen + 1 > max_gen && bnext > s) break;
+                const bool lazy = !KP.resident(r);
+                if (lazy && ngen + 1 > max_gen && bnext > s) break;
                 bsteps.push_back(r);
-                if (KP.needs_generation(r)) ngen++;
+                ngen += lazy;
             }
             bnext++;
         }
+        bstart.push_back(s);
+        bsteps_all.push_back(bsteps);
+    }
+    bstart.push_back(P);
+    for (size_t bi = 0; bi + 1 < bstart.size(); bi++) {
+        const int64_t s = bstart[bi], bnext = bstart[bi + 1];
+        const std::vector<u32>& bsteps = bsteps_all[bi];
         const int bn = (int)(bnext - s);
-        KP.release_except(bsteps);
         std::vector<const u64*> bkeys;
-        hs_status ks_ = KP.get(bsteps, bkeys);
+        hs_status ks_ = KP.acquire(bsteps, bkeys);
         if (ks_ != HS_OK) return ks_;
+        if (lazy_needed && bi + 2 < bstart.size()) {
+            ks_ = KP.prefetch(bsteps_all[bi + 1], bsteps);
+            if (ks_ != HS_OK) return ks_;
+        }
         for (int64_t t = s, k = -1; t < bnext; t++) {
             if (hR[t] && (k < 0 || bsteps[k] != hR[t])) k++;
             hK[t] = hR[t] ? bkeys[k] : nullptr;
@@ -405,7 +489,7 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, cons
                          strided(Fb + (size_t)z * ctL2, ctL2), ks, st);
         accumulate(d, z, L - 1, 2, strided(Cb, ctL2), out, st);
         accumulate(d, bn - z, L - 1, 2, strided(Fb + (size_t)z * ctL2, ctL2), out, st);
-        if (ngen) HS_CUDA(cudaStreamSynchronize(st));   // generated keys are freed next batch
+        KP.release(bsteps);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
