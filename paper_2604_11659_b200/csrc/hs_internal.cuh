@@ -58,6 +58,7 @@ struct hs_ctx {
     std::unordered_map<u32, Stream> lazy;    // registered steps generated on demand
     size_t keygen_batch = 16;                // keys generated per launch
     int64_t keys_generated = 0;
+    int* d_kg_err = nullptr;                 // set if a keygen stream window overflowed
     hs::KeyBuf relin;
     size_t batch_bytes = (size_t)6 << 30;   // runner work-buffer budget
     std::unordered_map<u32, hs::KeyBuf> galois;   // normalised step -> key
@@ -77,6 +78,8 @@ struct hs_ctx {
 
 namespace hs {
 // Generate Galois keys on the device into `dests` ([2][L+1][L+2][n] each).
+// Raises HS_EVAL_ERROR if any device key stream ran out of its window.
+hs_status keygen_check(hs_ctx* c);
 hs_status generate_galois_keys(hs_ctx* c, const std::vector<u32>& steps,
                                const std::vector<hs_ctx::Stream>& streams,
                                const std::vector<u64*>& dests, cudaStream_t st);

@@ -20,6 +20,7 @@
 // The SeedSequence -> PCG64 state and the ziggurat tables (read from the
 // installed numpy binary and validated against numpy on the host) are inputs.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "ops.cuh"
@@ -62,6 +63,8 @@ struct ZigTables {
 struct RngJump {                          // for t = 0..RNG_CH: A_t = M^t, S_t = sum_{k<t} M^k
     U128 A[RNG_CH + 1];
     U128 S[RNG_CH + 1];
+    U128 PA[64];                          // A_{2^j}
+    U128 PS[64];                          // S_{2^j}
 };
 
 struct KeyStream {
@@ -388,6 +391,318 @@ void keygen_streams(const Dev& d, int K, const void* streams, u64* const* a_out,
     note_launch();
 }
 
+// ====================================================== grid-parallel streams
+// The serial kernel above gives each key one SM.  Here all keys of a batch
+// advance through their streams in lockstep, one segment (one integers() or
+// normal() call) per pair of launches, and each segment is spread over
+// W / RNG_CH CTAs per key: a CTA jumps its key's PCG64 to its tile (binary
+// composition of power-of-two LCG jumps), generates the tile's draws, and
+// acceptance counts / ranks come from per-tile counts and block scans.  The
+// normal segment's token parse (fast tokens 1 draw, slow 2, tail 1+2k) is a
+// one-warp walk over the fast-path bitmap, skipping 32 fast draws per step.
+
+struct ParArgs {
+    const KeyStream* streams;
+    const RngJump* jump;
+    const ZigTables* zig;
+    const PrimeConst* pc;
+    const u64* thr;
+    u64* raw;              // [K][W] window draws
+    u32* cnt;              // [K][NT] per-tile counts (exclusive prefix after scan)
+    unsigned* fastb;       // [K][W/32]
+    unsigned* emitb;       // [K][W/32]
+    double* tailx;         // [K][W] values of tail tokens (sparse)
+    u64* pos_in;           // [K] segment start
+    u64* pos_out;          // [K] next segment start
+    u64* const* a_out;     // [K] a half of each key
+    long long* e_out;      // [K][L+1][n]
+    int* err;              // window overflow
+    int L, W, NT;
+    u32 n;
+};
+
+// State producing the draw at absolute position P + t + 1 ... : thread 0 jumps
+// the key's start state by P (power-of-two compositions), threads fan out.
+HS_DEV U128 tile_state(const ParArgs& A, const KeyStream& ks, u64 P, U128* s_x) {
+    const U128 inc{ks.inc_hi, ks.inc_lo};
+    if (threadIdx.x == 0) {
+        U128 x{ks.state_hi, ks.state_lo};
+        for (int j = 0; P; j++, P >>= 1)
+            if (P & 1) x = add128(mul128(A.jump->PA[j], x), mul128(A.jump->PS[j], inc));
+        *s_x = x;
+    }
+    __syncthreads();
+    const U128 x = *s_x;
+    return add128(mul128(A.jump->A[threadIdx.x + 1], x), mul128(A.jump->S[threadIdx.x + 1], inc));
+}
+
+// Generate the tile's draws; uniform mode counts Lemire accepts for bound
+// pc[sidx], normal mode writes the fast-path bitmap.
+__global__ void __launch_bounds__(RNG_T) pk_gen_kernel(ParArgs A, int normal, int sidx) {
+    __shared__ U128 s_x;
+    __shared__ u32 s_cnt[RNG_W];
+    const int k = blockIdx.y, tile = blockIdx.x;
+    const u32 t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const KeyStream ks = A.streams[k];
+    const U128 inc{ks.inc_hi, ks.inc_lo};
+    const u64 base = A.pos_in[k] + (u64)tile * RNG_CH;
+    U128 s = tile_state(A, ks, base, &s_x);
+    const U128 AT = A.jump->A[RNG_T], CT = mul128(A.jump->S[RNG_T], inc);
+    u64* raw = A.raw + (size_t)k * A.W + (size_t)tile * RNG_CH;
+    u32 c = 0;
+    const u64 q = A.pc[sidx].q, thr = A.thr[sidx];
+#pragma unroll
+    for (int e = 0; e < RNG_E; e++) {
+        const u32 i = e * RNG_T + t;
+        const u64 x = xsl_rr(s);
+        s = add128(mul128(s, AT), CT);
+        raw[i] = x;
+        if (normal) {
+            const u64 r8 = x >> 8;
+            const u64 rabs = (r8 >> 1) & 0x000fffffffffffffull;
+            const unsigned fb = __ballot_sync(0xffffffffu, rabs < A.zig->ki[x & 0xff]);
+            if (lane == 0) A.fastb[(size_t)k * (A.W / 32) + ((size_t)tile * RNG_CH + i) / 32] = fb;
+        } else {
+            c += __popc(__ballot_sync(0xffffffffu, x * q >= thr));
+        }
+    }
+    if (!normal) {
+        if (lane == 0) s_cnt[warp] = c;
+        __syncthreads();
+        if (t == 0) {
+            u32 tot = 0;
+            for (int w = 0; w < RNG_W; w++) tot += s_cnt[w];
+            A.cnt[(size_t)k * A.NT + tile] = tot;
+        }
+    }
+}
+
+// Uniform segment: write the first n accepted values in stream order.
+__global__ void __launch_bounds__(RNG_T) pk_uniform_write(ParArgs A, int digit, int sidx) {
+    __shared__ u32 cnt[RNG_E * RNG_W];
+    __shared__ u32 s_total, s_prefix;
+    const int k = blockIdx.y, tile = blockIdx.x;
+    const u32 t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const u32 n = A.n;
+    if (t == 0) {
+        u32 p = 0;
+        for (int j = 0; j < tile; j++) p += A.cnt[(size_t)k * A.NT + j];
+        s_prefix = p;
+        if (tile == A.NT - 1 && p + A.cnt[(size_t)k * A.NT + tile] < n) *A.err = 1;
+    }
+    __syncthreads();
+    const u32 prefix = s_prefix;
+    if (prefix >= n) return;
+    const u64 q = A.pc[sidx].q, thr = A.thr[sidx];
+    const u64* raw = A.raw + (size_t)k * A.W + (size_t)tile * RNG_CH;
+    unsigned ball[RNG_E];
+#pragma unroll
+    for (int e = 0; e < RNG_E; e++) {
+        ball[e] = __ballot_sync(0xffffffffu, raw[e * RNG_T + t] * q >= thr);
+        if (lane == 0) cnt[e * RNG_W + warp] = __popc(ball[e]);
+    }
+    chunk_scan(cnt, &s_total);
+    u64* dst = A.a_out[k] + ((size_t)digit * (A.L + 2) + sidx) * n;
+#pragma unroll
+    for (int e = 0; e < RNG_E; e++) {
+        if (!((ball[e] >> lane) & 1u)) continue;
+        const u32 idx = prefix + cnt[e * RNG_W + warp] + __popc(ball[e] & lt);
+        const u32 i = e * RNG_T + t;
+        if (idx < n) dst[idx] = __umul64hi(raw[i], q);
+        if (idx == n - 1) A.pos_out[k] = A.pos_in[k] + (u64)tile * RNG_CH + i + 1;
+    }
+}
+
+// Normal segment token walk (one warp per key) -> emit bitmap, tail values,
+// per-tile emit counts (exclusive prefix) and the next segment start.
+__global__ void pk_normal_walk(ParArgs A) {
+    const int k = blockIdx.x;
+    const u32 lane = threadIdx.x;
+    const u32 n = A.n;
+    const int words = A.W / 32;
+    const unsigned* fb = A.fastb + (size_t)k * words;
+    unsigned* eb = A.emitb + (size_t)k * words;
+    const u64* raw = A.raw + (size_t)k * A.W;
+    double* tx = A.tailx + (size_t)k * A.W;
+    for (int w = lane; w < words; w += 32) eb[w] = 0u;
+    __syncwarp();
+    if (lane == 0) {
+        u32 c = 0, cntv = 0;
+        bool done = false;
+        while (!done && c < (u32)A.W) {
+            // next non-fast position >= c
+            u32 s = (u32)A.W;
+            for (u32 w = c >> 5; w < (u32)words; w++) {
+                unsigned bits = ~fb[w];
+                if (w == (c >> 5)) bits &= ~((1u << (c & 31)) - 1u);
+                if (bits) {
+                    s = (w << 5) + __ffs(bits) - 1;
+                    break;
+                }
+            }
+            u32 run = s - c;
+            if (cntv + run >= n) {
+                run = n - cntv;
+                done = true;
+            }
+            set_bit_range(eb, c, c + run);
+            cntv += run;
+            c += run;
+            if (done || s >= (u32)A.W) break;
+            const u64 rs = raw[s];
+            const int zs = (int)(rs & 0xff);
+            const u64 rabs = ((rs >> 8) >> 1) & 0x000fffffffffffffull;
+            if (s + 2 >= (u32)A.W) break;                   // window exhausted
+            if (zs != 0) {
+                double xs = (double)rabs * A.zig->wi[zs];
+                if ((rs >> 8) & 1) xs = -xs;
+                const double u = next_double_of(raw[s + 1]);
+                if ((A.zig->fi[zs - 1] - A.zig->fi[zs]) * u + A.zig->fi[zs] < exp(-0.5 * xs * xs)) {
+                    eb[s >> 5] |= 1u << (s & 31);
+                    if (++cntv >= n) done = true;
+                }
+                c = s + 2;
+            } else {
+                u32 pos = s + 1;
+                double v = 0.0;
+                bool ok = false;
+                while (pos + 1 < (u32)A.W) {
+                    const double xx = -ZIG_INV_R * log1p(-next_double_of(raw[pos]));
+                    const double yy = -log1p(-next_double_of(raw[pos + 1]));
+                    pos += 2;
+                    if (yy + yy > xx * xx) {
+                        v = ((rabs >> 8) & 1) ? -(ZIG_R + xx) : ZIG_R + xx;
+                        ok = true;
+                        break;
+                    }
+                }
+                if (!ok) break;
+                tx[s] = v;
+                eb[s >> 5] |= 1u << (s & 31);
+                if (++cntv >= n) done = true;
+                c = pos;
+            }
+        }
+        if (!done) *A.err = 1;
+        A.pos_out[k] = A.pos_in[k] + c;
+    }
+    __syncwarp();
+    // exclusive per-tile prefix of emits (tiles of RNG_CH positions)
+    if (lane == 0) {
+        u32 run = 0;
+        for (int tile = 0; tile < A.NT; tile++) {
+            A.cnt[(size_t)k * A.NT + tile] = run;
+            for (int w = tile * (RNG_CH / 32); w < (tile + 1) * (RNG_CH / 32); w++) run += __popc(eb[w]);
+        }
+    }
+}
+
+// Normal segment: write e values (0 + 3.2 z, rint) of emitted tokens.
+__global__ void __launch_bounds__(RNG_T) pk_normal_write(ParArgs A, int digit) {
+    __shared__ u32 cnt[RNG_E * RNG_W];
+    __shared__ u32 s_total;
+    const int k = blockIdx.y, tile = blockIdx.x;
+    const u32 t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const u32 n = A.n;
+    const u32 prefix = A.cnt[(size_t)k * A.NT + tile];
+    if (prefix >= n) return;
+    const unsigned* eb = A.emitb + (size_t)k * (A.W / 32) + (size_t)tile * (RNG_CH / 32);
+    const u64* raw = A.raw + (size_t)k * A.W + (size_t)tile * RNG_CH;
+    const double* tx = A.tailx + (size_t)k * A.W + (size_t)tile * RNG_CH;
+    unsigned ball[RNG_E];
+#pragma unroll
+    for (int e = 0; e < RNG_E; e++) {
+        const u32 i = e * RNG_T + t;
+        ball[e] = __ballot_sync(0xffffffffu, (eb[i >> 5] >> (i & 31)) & 1u);
+        if (lane == 0) cnt[e * RNG_W + warp] = __popc(ball[e]);
+    }
+    chunk_scan(cnt, &s_total);
+    long long* dst = A.e_out + ((size_t)k * (A.L + 1) + digit) * n;
+#pragma unroll
+    for (int e = 0; e < RNG_E; e++) {
+        if (!((ball[e] >> lane) & 1u)) continue;
+        const u32 i = e * RNG_T + t;
+        const u32 idx = prefix + cnt[e * RNG_W + warp] + __popc(ball[e] & lt);
+        if (idx >= n) continue;
+        const u64 r = raw[i];
+        const int zi = (int)(r & 0xff);
+        const u64 rabs = ((r >> 8) >> 1) & 0x000fffffffffffffull;
+        double x;
+        if (zi == 0 && rabs >= A.zig->ki[0]) {
+            x = tx[i];                                   // tail token value
+        } else {
+            x = (double)rabs * A.zig->wi[zi];
+            if ((r >> 8) & 1) x = -x;
+        }
+        dst[idx] = (long long)rint(0.0 + 3.2 * x);
+    }
+}
+
+size_t keygen_par_window(u32 n) {
+    const size_t w = (size_t)n + n / 16 + 8192;
+    return (w + RNG_CH - 1) / RNG_CH * RNG_CH;
+}
+
+size_t keygen_par_scratch_bytes(int K, u32 n) {
+    const size_t W = keygen_par_window(n), NT = W / RNG_CH;
+    return (size_t)K * (W * 8 + W * 8 + W / 32 * 4 * 2 + NT * 4) + (size_t)K * 16 + 64;
+}
+
+// Replays K key streams in lockstep.  Returns false (nothing guaranteed) if
+// a window overflowed; the caller then falls back to the serial kernel.
+void keygen_streams_parallel(const Dev& d, int K, const void* streams, u64* const* a_out,
+                             long long* e_out, const void* jump, const void* zig, const u64* thr,
+                             void* scratch, int* err, cudaStream_t st) {
+    const int W = (int)keygen_par_window(d.n), NT = W / RNG_CH;
+    char* p = (char*)scratch;
+    ParArgs A{};
+    A.streams = (const KeyStream*)streams;
+    A.jump = (const RngJump*)jump;
+    A.zig = (const ZigTables*)zig;
+    A.pc = d.pc;
+    A.thr = thr;
+    A.raw = (u64*)p;
+    p += (size_t)K * W * 8;
+    A.tailx = (double*)p;
+    p += (size_t)K * W * 8;
+    A.fastb = (unsigned*)p;
+    p += (size_t)K * (W / 32) * 4;
+    A.emitb = (unsigned*)p;
+    p += (size_t)K * (W / 32) * 4;
+    A.cnt = (u32*)p;
+    p += (size_t)K * NT * 4;
+    u64* pos[2] = {(u64*)p, (u64*)p + K};
+    cudaMemsetAsync(pos[0], 0, (size_t)K * sizeof(u64), st);
+    A.a_out = a_out;
+    A.e_out = e_out;
+    A.err = err;
+    A.L = d.L;
+    A.W = W;
+    A.NT = NT;
+    A.n = d.n;
+    int cur = 0;
+    const dim3 grid(NT, K);
+    for (int digit = 0; digit <= d.L; digit++) {
+        for (int m = 0; m < d.L + 2; m++) {
+            A.pos_in = pos[cur];
+            A.pos_out = pos[cur ^ 1];
+            pk_gen_kernel<<<grid, RNG_T, 0, st>>>(A, 0, m);
+            pk_uniform_write<<<grid, RNG_T, 0, st>>>(A, digit, m);
+            note_launch(2);
+            cur ^= 1;
+        }
+        A.pos_in = pos[cur];
+        A.pos_out = pos[cur ^ 1];
+        pk_gen_kernel<<<grid, RNG_T, 0, st>>>(A, 1, 0);
+        pk_normal_walk<<<K, 32, 0, st>>>(A);
+        pk_normal_write<<<grid, RNG_T, 0, st>>>(A, digit);
+        note_launch(3);
+        cur ^= 1;
+    }
+}
+
 void ksk_galois_combine(const Dev& d, int K, u64* const* keys, const u32* gal, const u64* sk,
                         const ulonglong2* f, cudaStream_t st) {
     dim3 g((d.n + 255) / 256, (d.L + 1) * (d.L + 2), K);
@@ -524,6 +839,15 @@ hs_status ensure_keygen_tables(hs_ctx* c) {
         s += a;
         a *= PCG_MULT;
     }
+    {   // power-of-two jumps: (A,S)_{2^(j+1)} = (A^2, S + A S)
+        u128h pa = PCG_MULT, ps = 1;
+        for (int j = 0; j < 64; j++) {
+            J->PA[j] = U128{(u64)(pa >> 64), (u64)pa};
+            J->PS[j] = U128{(u64)(ps >> 64), (u64)ps};
+            ps = ps + pa * ps;
+            pa = pa * pa;
+        }
+    }
     std::vector<u64> thr(L + 2);
     for (int p = 0; p < L + 2; p++) {
         const u64 q = c->primes[p];
@@ -568,6 +892,18 @@ u64 powmod_u(u64 b, u64 e, u64 q) {
 
 namespace hs {
 
+hs_status keygen_check(hs_ctx* c) {
+    if (!c->d_kg_err) return HS_OK;
+    int err = 0;
+    HS_CUDA(cudaMemcpy(&err, c->d_kg_err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (err) {
+        cudaMemset(c->d_kg_err, 0, sizeof(int));
+        set_error("device key stream exceeded its window (rerun with HS_KEYGEN_SERIAL=1)");
+        return HS_EVAL_ERROR;
+    }
+    return HS_OK;
+}
+
 // Generate keys for `steps` (PCG64 start states `streams`) into `dests`
 // (each a [2][L+1][L+2][n] buffer).  Used eagerly (hs_key_generate_galois)
 // and lazily by the runner for keys it was told how to make.
@@ -594,6 +930,15 @@ hs_status generate_galois_keys(hs_ctx* c, const std::vector<u32>& steps,
     HS_CUDA(cudaMallocAsync((void**)&d_aout, KB * sizeof(u64*), st));
     HS_CUDA(cudaMallocAsync((void**)&d_gal, KB * sizeof(u32), st));
     HS_CUDA(cudaMallocAsync((void**)&d_streams, KB * sizeof(hs_ctx::Stream), st));
+    static const bool serial = getenv("HS_KEYGEN_SERIAL") != nullptr;
+    void* par_scratch = nullptr;
+    if (!serial) {
+        if (!c->d_kg_err) {
+            HS_CUDA(cudaMalloc((void**)&c->d_kg_err, sizeof(int)));
+            HS_CUDA(cudaMemset(c->d_kg_err, 0, sizeof(int)));
+        }
+        HS_CUDA(cudaMallocAsync(&par_scratch, keygen_par_scratch_bytes(KB, c->n), st));
+    }
     for (size_t k0 = 0; k0 < steps.size(); k0 += KB) {
         const int K = (int)std::min<size_t>(KB, steps.size() - k0);
         std::vector<u64*> keys(K), aout(K);
@@ -608,11 +953,16 @@ hs_status generate_galois_keys(hs_ctx* c, const std::vector<u32>& steps,
         HS_CUDA(cudaMemcpyAsync(d_gal, gal.data(), K * sizeof(u32), cudaMemcpyHostToDevice, st));
         HS_CUDA(cudaMemcpyAsync(d_streams, streams.data() + k0, K * sizeof(hs_ctx::Stream),
                                 cudaMemcpyHostToDevice, st));
-        keygen_streams(c->dev, K, d_streams, d_aout, e, c->d_jump, c->d_zig, c->d_thr, st);
+        if (par_scratch)
+            keygen_streams_parallel(c->dev, K, d_streams, d_aout, e, c->d_jump, c->d_zig, c->d_thr,
+                                    par_scratch, c->d_kg_err, st);
+        else
+            keygen_streams(c->dev, K, d_streams, d_aout, e, c->d_jump, c->d_zig, c->d_thr, st);
         keygen_assemble(c->dev, K, d_keys, e, d_gal, c->d_sk, c->d_kskf, st);
         // pageable host staging is copied at call time; device arrays are stream-ordered
         c->keys_generated += K;
     }
+    if (par_scratch) cudaFreeAsync(par_scratch, st);
     cudaFreeAsync(e, st);
     cudaFreeAsync(d_keys, st);
     cudaFreeAsync(d_aout, st);
@@ -659,8 +1009,19 @@ hs_status hs_keygen_register(hs_ctx* c, const uint32_t* steps, const uint64_t* s
     return HS_OK;
 }
 
+hs_status hs_key_generate_galois_impl(hs_ctx* c, const uint32_t* steps, const uint64_t* states,
+                                      int32_t nsteps, void* stream);
+
 hs_status hs_key_generate_galois(hs_ctx* c, const uint32_t* steps, const uint64_t* states, int32_t nsteps,
                                  void* stream) {
+    hs_status s = hs_key_generate_galois_impl(c, steps, states, nsteps, stream);
+    if (s != HS_OK) return s;
+    HS_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    return keygen_check(c);
+}
+
+hs_status hs_key_generate_galois_impl(hs_ctx* c, const uint32_t* steps, const uint64_t* states,
+                                      int32_t nsteps, void* stream) {
     std::vector<u32> st(steps, steps + nsteps);
     std::vector<hs_ctx::Stream> ss(nsteps);
     std::vector<u64*> dests(nsteps);

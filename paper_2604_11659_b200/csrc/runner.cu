@@ -496,6 +496,11 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, cons
         set_error(std::string("kernel launch failed: ") + cudaGetErrorString(e));
         return (hs_status)HS_CUDA_ERROR;
     }
+    if (lazy_needed) {            // generated keys must have come from complete streams
+        HS_CUDA(cudaStreamSynchronize(st));
+        hs_status ks_ = keygen_check(c);
+        if (ks_ != HS_OK) return ks_;
+    }
     *cnt = C;
     return (hs_status)HS_OK;
 }
