@@ -673,6 +673,7 @@ void keygen_streams_parallel(const Dev& d, int K, const void* streams, u64* cons
     p += (size_t)K * (W / 32) * 4;
     A.cnt = (u32*)p;
     p += (size_t)K * NT * 4;
+    p = (char*)(((uintptr_t)p + 15) & ~(uintptr_t)15);     // K * NT may be odd
     u64* pos[2] = {(u64*)p, (u64*)p + K};
     cudaMemsetAsync(pos[0], 0, (size_t)K * sizeof(u64), st);
     A.a_out = a_out;

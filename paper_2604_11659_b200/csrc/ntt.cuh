@@ -40,7 +40,7 @@ HS_DEV u32 spad(u32 i) { return i + (i >> 3); }
 // the round's bits (smem stride S = 2^LOWB * C); each thread owns 8 / 2^R
 // units.  The round schedule (ntt_rounds_*) keeps LOWB = 0 or LOWB >= 3, so
 // the padded smem index of a unit's elements is affine: base + e * PS.
-template <bool FWD, int LOGG, int H, int C, int A, int R>
+template <bool FWD, bool LZ, int LOGG, int H, int C, int A, int R>
 __device__ __forceinline__ void ntt_round(u64* sm, const ulonglong2* __restrict__ tw, u32 hi0,
                                           int s0, u64 q, u64 two_q) {
     constexpr int G = 1 << LOGG;
@@ -71,13 +71,13 @@ __device__ __forceinline__ void ntt_round(u64* sm, const ulonglong2* __restrict_
 #pragma unroll
             for (int j = 0; j < R; j++) {
                 const int ls = A + j;
-                const u32 tb = (1u << (s0 + ls)) + (hi << ls) + (go_high << j);
+                const ulonglong2* __restrict__ twb = tw + ((1u << (s0 + ls)) + (hi << ls) + (go_high << j));
 #pragma unroll
                 for (int e = 0; e < NU; e++) {
                     const int bit = 1 << (R - 1 - j);
                     if (e & bit) continue;
-                    const ulonglong2 w = tw[tb + (e >> (R - j))];
-                    const u64 x = csub(v[e], two_q);
+                    const ulonglong2 w = twb[e >> (R - j)];
+                    const u64 x = LZ ? v[e] : csub(v[e], two_q);
                     const u64 t = shoup_lazy(v[e + bit], w.x, w.y, q);
                     v[e] = x + t;
                     v[e + bit] = x - t + two_q;
@@ -87,12 +87,12 @@ __device__ __forceinline__ void ntt_round(u64* sm, const ulonglong2* __restrict_
 #pragma unroll
             for (int j = R - 1; j >= 0; j--) {
                 const int ls = A + j;
-                const u32 tb = (1u << (s0 + ls)) + (hi << ls) + (go_high << j);
+                const ulonglong2* __restrict__ twb = tw + ((1u << (s0 + ls)) + (hi << ls) + (go_high << j));
 #pragma unroll
                 for (int e = 0; e < NU; e++) {
                     const int bit = 1 << (R - 1 - j);
                     if (e & bit) continue;
-                    const ulonglong2 w = tw[tb + (e >> (R - j))];
+                    const ulonglong2 w = twb[e >> (R - j)];
                     const u64 x = v[e], y = v[e + bit];
                     v[e] = csub(x + y, two_q);
                     v[e + bit] = shoup_lazy(x - y + two_q, w.x, w.y, q);
@@ -117,14 +117,14 @@ struct RoundPlan {
     static constexpr int width(int r) { return REM == 0 ? 3 : (r == F - 1 ? REM : 3); }
 };
 
-template <int LOGG, int H, int C, int RI>
+template <int LOGG, int H, int C, bool LZ, int RI>
 __device__ __forceinline__ void ntt_rounds_fwd_from(u64* sm, const ulonglong2* tw, u32 hi0, int s0,
                                                     u64 q, u64 two_q) {
     if constexpr (RI < RoundPlan<LOGG>::count()) {
-        ntt_round<true, LOGG, H, C, RoundPlan<LOGG>::start(RI), RoundPlan<LOGG>::width(RI)>(
+        ntt_round<true, LZ, LOGG, H, C, RoundPlan<LOGG>::start(RI), RoundPlan<LOGG>::width(RI)>(
             sm, tw, hi0, s0, q, two_q);
         __syncthreads();
-        ntt_rounds_fwd_from<LOGG, H, C, RI + 1>(sm, tw, hi0, s0, q, two_q);
+        ntt_rounds_fwd_from<LOGG, H, C, LZ, RI + 1>(sm, tw, hi0, s0, q, two_q);
     }
 }
 
@@ -132,18 +132,28 @@ template <int LOGG, int H, int C, int RI>
 __device__ __forceinline__ void ntt_rounds_inv_from(u64* sm, const ulonglong2* tw, u32 hi0, int s0,
                                                     u64 q, u64 two_q) {
     if constexpr (RI >= 0) {
-        ntt_round<false, LOGG, H, C, RoundPlan<LOGG>::start(RI), RoundPlan<LOGG>::width(RI)>(
+        ntt_round<false, false, LOGG, H, C, RoundPlan<LOGG>::start(RI), RoundPlan<LOGG>::width(RI)>(
             sm, tw, hi0, s0, q, two_q);
         __syncthreads();
         ntt_rounds_inv_from<LOGG, H, C, RI - 1>(sm, tw, hi0, s0, q, two_q);
     }
 }
 
-template <int LOGG, int H, int C>
+// LZ: skip the per-butterfly reduction of the upper input (values grow by
+// < 2q per stage; only for primes with fwd_lazy_ok()).
+template <int LOGG, int H, int C, bool LZ = false>
 __device__ __forceinline__ void ntt_rounds_fwd(u64* sm, const ulonglong2* tw, u32 hi0, int s0, u64 q,
                                                u64 two_q) {
-    ntt_rounds_fwd_from<LOGG, H, C, 0>(sm, tw, hi0, s0, q, two_q);
+    ntt_rounds_fwd_from<LOGG, H, C, LZ, 0>(sm, tw, hi0, s0, q, two_q);
 }
+
+// Forward passes may run fully lazy when every intermediate stays below
+// 2^64: inputs < 4q, each of <= 17 stages adds < 2q, so < 38q < 2^64 for
+// q < 2^58 (the ~50-bit chain primes; the 60-bit q_0 and aux keep Harvey's
+// per-butterfly reduction).  Lazy outputs are brought to [0, 2q) with
+// reduce64_lazy before a job's store() sees them.
+HS_DEV bool fwd_lazy_ok(const PrimeConst& P) { return P.q < (1ull << 58); }
+HS_DEV u64 reduce64_lazy(u64 t, const PrimeConst& P) { return t - mulhi64(t, P.m64) * P.q; }
 
 template <int LOGG, int H, int C>
 __device__ __forceinline__ void ntt_rounds_inv(u64* sm, const ulonglong2* tw, u32 hi0, int s0, u64 q,
@@ -192,12 +202,21 @@ ntt_pass_kernel(Dev d, Job job, int s0, int jbase) {
         for (int k = 0; k < NTT_EPT; k++) sm[spad(t + k * T)] = src[j0 + k * jstep];
     }
     __syncthreads();
-    if (FWD) ntt_rounds_fwd<LOGG, H, C>(sm, tw, hi0, s0, P.q, P.two_q);
-    else ntt_rounds_inv<LOGG, H, C>(sm, tw, hi0, s0, P.q, P.two_q);
+    const bool lz = FWD && fwd_lazy_ok(P);
+    if (FWD) {
+        if (lz) ntt_rounds_fwd<LOGG, H, C, true>(sm, tw, hi0, s0, P.q, P.two_q);
+        else ntt_rounds_fwd<LOGG, H, C, false>(sm, tw, hi0, s0, P.q, P.two_q);
+    } else {
+        ntt_rounds_inv<LOGG, H, C>(sm, tw, hi0, s0, P.q, P.two_q);
+    }
 
     if (LAST) {
 #pragma unroll
-        for (int k = 0; k < NTT_EPT; k++) job.store(jc, j0 + k * jstep, sm[spad(t + k * T)], P);
+        for (int k = 0; k < NTT_EPT; k++) {
+            u64 v = sm[spad(t + k * T)];
+            if (FWD && lz) v = reduce64_lazy(v, P);
+            job.store(jc, j0 + k * jstep, v, P);
+        }
     } else {
         u64* __restrict__ dst = job.scratch(jc);
 #pragma unroll
