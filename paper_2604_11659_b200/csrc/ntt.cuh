@@ -11,12 +11,18 @@
 // Tiling: a pass covers a contiguous range of stages [s0, s0+LOGG).  Those
 // stages only mix indices that differ in bits [log n - s0 - LOGG, log n - s0),
 // so the limb splits into independent groups of G = 2^LOGG elements.  One CTA
-// stages H x G x C elements in shared memory: H consecutive "hi" values
-// (bits above the range) and C consecutive "lo" columns (bits below it).
-// n <= 2^11 runs as one pass (whole limb per CTA); larger limbs run as two
-// passes (strided column pass + contiguous row pass), in place in the
-// destination buffer.  Values stay lazy between stages: [0,4q) forward
-// (Harvey), [0,2q) inverse; Shoup products with precomputed twiddle pairs.
+// owns H x G x C elements: H consecutive "hi" values (bits above the range)
+// and C consecutive "lo" columns (bits below it).  n <= 2^11 runs as one pass
+// (whole limb per CTA); larger limbs run as two passes (strided column pass +
+// contiguous row pass), in place in the destination buffer.
+//
+// Two engines share the butterfly helpers:
+//  * PassEngine (ntt_pass_kernel): radix-16 register rounds, 16 elements per
+//    thread, the first/last round talking to global memory directly when that
+//    is coalesced, one padded shared-memory exchange per round boundary.
+//  * the radix-8 shared-memory rounds (ntt_round*), kept for the fused
+//    ModUp + key inner-product kernel (ops.cu) whose 128-bit accumulators
+//    leave no registers for 16 elements per thread.
 //
 // A "Job" functor supplies, per batch entry (blockIdx.y): prime(), the
 // first-pass load(), the last-pass store(), and scratch() -- the limb buffer
@@ -27,20 +33,49 @@
 
 namespace hs {
 
-constexpr int NTT_TILE = 2048;      // elements per CTA tile (16 KiB smem + padding)
-constexpr int NTT_EPT = 8;          // elements per thread (radix-8 register rounds)
+constexpr int NTT_TILE = 2048;      // elements per CTA tile (16 KiB + padding)
+
+// ======================================================= modular helpers
+// x - m if x >= m (x, m < 2^63): sign test on the difference.
+HS_DEV u64 csub_s(u64 x, u64 m) {
+    const u64 d = x - m;
+    return (long long)d < 0 ? x : d;
+}
+
+HS_DEV u64 mulhi_ex(u64 x, u64 y) { return __umul64hi(x, y); }
+
+// hi64(x*y) minus 0, 1 or 2: drops the low x0*y0 product and the low halves
+// of the two cross products (each dropped part is < one unit of 2^64).
+HS_DEV u64 mulhi_apx(u64 x, u64 y) {
+    const u32 x0 = (u32)x, x1 = (u32)(x >> 32), y0 = (u32)y, y1 = (u32)(y >> 32);
+    const u64 r = (u64)x1 * y1 + __umulhi(x1, y0);
+    return r + __umulhi(x0, y1);
+}
+
+// Shoup products x*w mod q given w_sh = floor(w 2^64 / q), any x < 2^64:
+// exact quotient estimate -> [0, 2q); approximate -> [0, 4q).
+// x*w - Q*q is formed as x*w + Q*(2^64 - q) (nq) so the chain is pure IMADs.
+HS_DEV u64 shoup_ex(u64 x, u64 w, u64 w_sh, u64 nq) { return x * w + mulhi_ex(x, w_sh) * nq; }
+HS_DEV u64 shoup_ax(u64 x, u64 w, u64 w_sh, u64 nq) { return x * w + mulhi_apx(x, w_sh) * nq; }
+
+// Forward passes run fully lazy ("LZ") when every intermediate stays far
+// below 2^63: inputs < 4q, each of <= 17 stages adds < 4q (approximate Shoup),
+// so values stay < 72q < 2^63 for q < 2^56 (the ~50-bit chain primes).  The
+// 60-bit q_0 and aux prime keep Harvey's [0, 4q) butterflies.  Lazy outputs
+// reach a job's store() in [0, 4q) via reduce64_lazy (any t < 2^64).
+HS_DEV bool fwd_lazy_ok(const PrimeConst& P) { return P.q < (1ull << 56); }
+HS_DEV u64 reduce64_lazy(u64 t, const PrimeConst& P) { return t - mulhi_apx(t, P.m64) * P.q; }
+
+// ======================================================= radix-8 smem rounds
+constexpr int NTT_EPT = 8;          // elements per thread
 constexpr int NTT_THREADS = NTT_TILE / NTT_EPT;
 
-// Shared-memory index with one pad word per 8 (keeps the stride-8 accesses of
-// the lowest-bit round at the 2-wavefront minimum).
+// Shared-memory index with one pad word per 8.
 HS_DEV u32 spad(u32 i) { return i + (i >> 3); }
 
 // One register round: local stages [A, A+R) of a tile with H rows, G = 2^LOGG
-// group elements and C columns.  A "unit" is the 2^R elements that differ in
-// the round's bits (smem stride S = 2^LOWB * C); each thread owns 8 / 2^R
-// units.  The round schedule (ntt_rounds_*) keeps LOWB = 0 or LOWB >= 3, so
-// the padded smem index of a unit's elements is affine: base + e * PS.
-template <bool FWD, bool LZ, int LOGG, int H, int C, int A, int R>
+// group elements and C columns, read from and written back to shared memory.
+template <bool FWD, int LOGG, int H, int C, int A, int R>
 __device__ __forceinline__ void ntt_round(u64* sm, const ulonglong2* __restrict__ tw, u32 hi0,
                                           int s0, u64 q, u64 two_q) {
     constexpr int G = 1 << LOGG;
@@ -52,6 +87,7 @@ __device__ __forceinline__ void ntt_round(u64* sm, const ulonglong2* __restrict_
     constexpr int S = (1 << LOWB) * C;
     static_assert(S % 8 == 0 || (S == 1 && R == 3), "round schedule must keep smem affine");
     constexpr int PS = S % 8 == 0 ? S + S / 8 : 1;
+    const u64 nq = 0ull - q;
 #pragma unroll
     for (int k = 0; k < UPT; k++) {
         const u32 U = threadIdx.x + k * T;
@@ -67,35 +103,25 @@ __device__ __forceinline__ void ntt_round(u64* sm, const ulonglong2* __restrict_
         u64 v[NU];
 #pragma unroll
         for (int e = 0; e < NU; e++) v[e] = sm[base + e * PS];
-        if (FWD) {
 #pragma unroll
-            for (int j = 0; j < R; j++) {
-                const int ls = A + j;
-                const ulonglong2* __restrict__ twb = tw + ((1u << (s0 + ls)) + (hi << ls) + (go_high << j));
+        for (int jj = 0; jj < R; jj++) {
+            const int j = FWD ? jj : R - 1 - jj;
+            const int ls = A + j;
+            const ulonglong2* __restrict__ twb = tw + ((1u << (s0 + ls)) + (hi << ls) + (go_high << j));
+            const int bit = 1 << (R - 1 - j);
 #pragma unroll
-                for (int e = 0; e < NU; e++) {
-                    const int bit = 1 << (R - 1 - j);
-                    if (e & bit) continue;
-                    const ulonglong2 w = twb[e >> (R - j)];
-                    const u64 x = LZ ? v[e] : csub(v[e], two_q);
-                    const u64 t = shoup_lazy(v[e + bit], w.x, w.y, q);
+            for (int e = 0; e < NU; e++) {
+                if (e & bit) continue;
+                const ulonglong2 w = twb[e >> (R - j)];
+                if (FWD) {
+                    const u64 x = csub_s(v[e], two_q);
+                    const u64 t = shoup_ex(v[e + bit], w.x, w.y, nq);
                     v[e] = x + t;
                     v[e + bit] = x - t + two_q;
-                }
-            }
-        } else {
-#pragma unroll
-            for (int j = R - 1; j >= 0; j--) {
-                const int ls = A + j;
-                const ulonglong2* __restrict__ twb = tw + ((1u << (s0 + ls)) + (hi << ls) + (go_high << j));
-#pragma unroll
-                for (int e = 0; e < NU; e++) {
-                    const int bit = 1 << (R - 1 - j);
-                    if (e & bit) continue;
-                    const ulonglong2 w = twb[e >> (R - j)];
+                } else {
                     const u64 x = v[e], y = v[e + bit];
-                    v[e] = csub(x + y, two_q);
-                    v[e + bit] = shoup_lazy(x - y + two_q, w.x, w.y, q);
+                    v[e] = csub_s(x + y, two_q);
+                    v[e + bit] = shoup_ex(x - y + two_q, w.x, w.y, nq);
                 }
             }
         }
@@ -109,7 +135,6 @@ __device__ __forceinline__ void ntt_round(u64* sm, const ulonglong2* __restrict_
 template <int LOGG>
 struct RoundPlan {
     static constexpr int F = LOGG / 3, REM = LOGG % 3;
-    // start stage and width of round number r (0-based, forward order)
     static constexpr int count() { return F + (REM ? 1 : 0); }
     static constexpr int start(int r) {
         return REM == 0 ? 3 * r : (r < F - 1 ? 3 * r : (r == F - 1 ? 3 * (F - 1) : LOGG - 3));
@@ -117,119 +142,292 @@ struct RoundPlan {
     static constexpr int width(int r) { return REM == 0 ? 3 : (r == F - 1 ? REM : 3); }
 };
 
-template <int LOGG, int H, int C, bool LZ, int RI>
+template <int LOGG, int H, int C, int RI>
 __device__ __forceinline__ void ntt_rounds_fwd_from(u64* sm, const ulonglong2* tw, u32 hi0, int s0,
                                                     u64 q, u64 two_q) {
     if constexpr (RI < RoundPlan<LOGG>::count()) {
-        ntt_round<true, LZ, LOGG, H, C, RoundPlan<LOGG>::start(RI), RoundPlan<LOGG>::width(RI)>(
+        ntt_round<true, LOGG, H, C, RoundPlan<LOGG>::start(RI), RoundPlan<LOGG>::width(RI)>(
             sm, tw, hi0, s0, q, two_q);
         __syncthreads();
-        ntt_rounds_fwd_from<LOGG, H, C, LZ, RI + 1>(sm, tw, hi0, s0, q, two_q);
+        ntt_rounds_fwd_from<LOGG, H, C, RI + 1>(sm, tw, hi0, s0, q, two_q);
     }
 }
 
-template <int LOGG, int H, int C, int RI>
-__device__ __forceinline__ void ntt_rounds_inv_from(u64* sm, const ulonglong2* tw, u32 hi0, int s0,
-                                                    u64 q, u64 two_q) {
-    if constexpr (RI >= 0) {
-        ntt_round<false, false, LOGG, H, C, RoundPlan<LOGG>::start(RI), RoundPlan<LOGG>::width(RI)>(
-            sm, tw, hi0, s0, q, two_q);
-        __syncthreads();
-        ntt_rounds_inv_from<LOGG, H, C, RI - 1>(sm, tw, hi0, s0, q, two_q);
-    }
-}
-
-// LZ: skip the per-butterfly reduction of the upper input (values grow by
-// < 2q per stage; only for primes with fwd_lazy_ok()).
-template <int LOGG, int H, int C, bool LZ = false>
+// Forward stages [s0, s0+LOGG) of a tile held in shared memory (inputs < 4q,
+// outputs in [0, 4q)).
+template <int LOGG, int H, int C>
 __device__ __forceinline__ void ntt_rounds_fwd(u64* sm, const ulonglong2* tw, u32 hi0, int s0, u64 q,
                                                u64 two_q) {
-    ntt_rounds_fwd_from<LOGG, H, C, LZ, 0>(sm, tw, hi0, s0, q, two_q);
+    ntt_rounds_fwd_from<LOGG, H, C, 0>(sm, tw, hi0, s0, q, two_q);
 }
 
-// Forward passes may run fully lazy when every intermediate stays below
-// 2^64: inputs < 4q, each of <= 17 stages adds < 2q, so < 38q < 2^64 for
-// q < 2^58 (the ~50-bit chain primes; the 60-bit q_0 and aux keep Harvey's
-// per-butterfly reduction).  Lazy outputs are brought to [0, 2q) with
-// reduce64_lazy before a job's store() sees them.
-HS_DEV bool fwd_lazy_ok(const PrimeConst& P) { return P.q < (1ull << 58); }
-HS_DEV u64 reduce64_lazy(u64 t, const PrimeConst& P) { return t - mulhi64(t, P.m64) * P.q; }
+// ======================================================= radix-16 engine
+// A pass of LOGG stages is split into register rounds of <= 4 stages (<= 3
+// when EPT = 8).  Each thread holds EPT elements; in round r it owns
+// EPT / 2^R "units" -- the 2^R elements that differ only in the round's bits
+// -- and performs all their butterflies in registers.
+constexpr int NTT_EPT16 = 16;
 
-template <int LOGG, int H, int C>
-__device__ __forceinline__ void ntt_rounds_inv(u64* sm, const ulonglong2* tw, u32 hi0, int s0, u64 q,
-                                               u64 two_q) {
-    ntt_rounds_inv_from<LOGG, H, C, RoundPlan<LOGG>::count() - 1>(sm, tw, hi0, s0, q, two_q);
+template <int LOGG, int EPT>
+struct Plan {
+    static constexpr int MAXR = EPT >= 16 ? 4 : 3;
+    static constexpr int count() { return LOGG <= MAXR ? 1 : (LOGG + MAXR - 1) / MAXR; }
+    static constexpr int width(int r) { return LOGG / count() + (r < LOGG % count() ? 1 : 0); }
+    static constexpr int start(int r) {
+        int a = 0;
+        for (int i = 0; i < r; i++) a += width(i);
+        return a;
+    }
+};
+
+// Padded shared-memory index (one pad word per 16 u64): with the unit
+// mappings below, 16 consecutive lanes hit 16 distinct 8-byte bank pairs.
+HS_DEV u32 spad16(u32 i) { return i + (i >> 4); }
+
+template <int LOGG, int H, int C, int EPT, int A, int R>
+struct RoundMap {
+    static constexpr int G = 1 << LOGG;
+    static constexpr int TILE = H * G * C;
+    static constexpr int T = TILE / EPT;
+    static constexpr int RR = R;
+    static constexpr int AA = A;
+    static constexpr int NU = 1 << R;
+    static constexpr int UPT = EPT / NU;
+    static constexpr int LOWB = LOGG - A - R;
+    static constexpr int S = (1 << LOWB) * C;          // tile-index stride of a unit
+    // Unit elements differ only in tile-index bits that are zero in the unit
+    // base, so their padded offsets are compile-time constants.
+    static constexpr u32 off(int e) { return (u32)(e * S + ((e * S) >> 4)); }
+    // Consecutive threads touch runs of >= 4 consecutive global elements.
+    static constexpr bool direct = C >= 4 || LOWB >= 2;
+    struct Unit {
+        u32 base;    // tile index of element 0
+        u32 h;       // row within the tile
+        u32 g;       // group index of element 0
+        u32 c;       // column
+        u32 gh;      // group bits above the round
+    };
+    HS_DEV static Unit unit(u32 U) {
+        Unit u;
+        u.c = U % C;
+        const u32 rest = U / C;
+        const u32 go = rest % (G >> R);
+        u.h = rest / (G >> R);
+        u.gh = go >> LOWB;
+        u.g = (u.gh << (LOWB + R)) | (go & ((1u << LOWB) - 1u));
+        u.base = (u.h * G + u.g) * C + u.c;
+        return u;
+    }
+};
+
+// Butterflies of one unit (2^R values in v[]).  Twiddle of local stage j,
+// element e: tw[(Y << j) + (e >> (R - j))] with Y = ((2^s0 + hi) << A) + gh,
+// i.e. roots[m + block] of the reference loop (_fast.pyx:55-66).
+template <bool FWD, bool LZ, int R>
+HS_DEV void unit_butterflies(u64* v, const ulonglong2* __restrict__ tw, u32 Y, u64 nq, u64 two_q,
+                             u64 four_q) {
+    constexpr int NU = 1 << R;
+#pragma unroll
+    for (int jj = 0; jj < R; jj++) {
+        const int j = FWD ? jj : R - 1 - jj;
+        const ulonglong2* __restrict__ twp = tw + (Y << j);
+        const int bit = 1 << (R - 1 - j);
+#pragma unroll
+        for (int e = 0; e < NU; e++) {
+            if (e & bit) continue;
+            const ulonglong2 w = twp[e >> (R - j)];
+            if (FWD && LZ) {
+                const u64 x = v[e];
+                const u64 t = shoup_ax(v[e + bit], w.x, w.y, nq);          // [0, 4q)
+                v[e] = x + t;
+                v[e + bit] = x - t + four_q;
+            } else if (FWD) {
+                const u64 x = csub_s(v[e], two_q);                        // [0, 2q)
+                const u64 t = shoup_ex(v[e + bit], w.x, w.y, nq);          // [0, 2q)
+                v[e] = x + t;
+                v[e + bit] = x - t + two_q;
+            } else {
+                const u64 x = v[e], y = v[e + bit];                      // [0, 2q)
+                v[e] = csub_s(x + y, two_q);
+                v[e + bit] = shoup_ex(x - y + two_q, w.x, w.y, nq);
+            }
+        }
+    }
 }
 
 // Job interface: `typename Job::Ctx ctx = job.make(jb)` is evaluated once per
 // CTA (pointer-table lookups, index decoding), then prime(ctx),
-// load(ctx, j, P), scratch(ctx), store(ctx, j, v, P) per element.
-template <bool FWD, bool FIRST, bool LAST, int LOGG, int H, int C, class Job>
-__global__ void __launch_bounds__(NTT_THREADS)
-ntt_pass_kernel(Dev d, Job job, int s0, int jbase) {
-    constexpr int G = 1 << LOGG;
-    constexpr int TILE = H * G * C;
-    constexpr int T = TILE / NTT_EPT;
-    __shared__ u64 sm[TILE + TILE / 8];
+// load(ctx, j, P), scratch(ctx), store(ctx, j, v, P) per element.  load()
+// returns [0, q) (forward loads may return up to 4q); store() receives
+// [0, 4q) forward and [0, 2q) inverse.
+template <bool FWD, bool FIRST, bool LAST, int LOGG, int H, int C, int EPT, class Job>
+struct PassEngine {
+    using PL = Plan<LOGG, EPT>;
+    static constexpr int G = 1 << LOGG;
+    static constexpr int TILE = H * G * C;
+    static constexpr int T = TILE / EPT;
+    static constexpr int NR = PL::count();
+    static constexpr int SMW = TILE + TILE / 16;       // padded words per buffer
+    template <int r>
+    using RM = RoundMap<LOGG, H, C, EPT, PL::start(r), PL::width(r)>;
+    static constexpr int RFIRST = FWD ? 0 : NR - 1;
+    static constexpr int RLAST = FWD ? NR - 1 : 0;
 
-    const int log_n = d.log_n;
-    const int lo_bits = log_n - s0 - LOGG;
-    const int jb = jbase + (int)blockIdx.y;
-    const typename Job::Ctx jc = job.make(jb);
-    const int p = job.prime(jc);
-    const PrimeConst P = d.pc[p];
-    const ulonglong2* __restrict__ tw = (FWD ? d.tw : d.itw) + (size_t)p * d.n;
-
-    const u32 ncolblk = (1u << lo_bits) / C;
-    const u32 hi0 = (blockIdx.x / ncolblk) * H;
-    const u32 lo0 = (blockIdx.x % ncolblk) * C;
-
-    // element e = t + k*T of the tile sits at global index j0 + k*jstep
-    auto gidx = [&](u32 e) -> u32 {
-        u32 c = e % C, g = (e / C) % G, h = e / (C * G);
-        return ((hi0 + h) << (log_n - s0)) | (g << lo_bits) | (lo0 + c);
-    };
-    const u32 t = threadIdx.x;
-    const u32 j0 = gidx(t);
-    const u32 jstep = NTT_EPT > 1 ? gidx(t + T) - j0 : 0;
-
-    if (FIRST) {
-#pragma unroll
-        for (int k = 0; k < NTT_EPT; k++) sm[spad(t + k * T)] = job.load(jc, j0 + k * jstep, P);
-    } else {
-        const u64* __restrict__ src = job.scratch(jc);
-#pragma unroll
-        for (int k = 0; k < NTT_EPT; k++) sm[spad(t + k * T)] = src[j0 + k * jstep];
-    }
-    __syncthreads();
-    const bool lz = FWD && fwd_lazy_ok(P);
-    if (FWD) {
-        if (lz) ntt_rounds_fwd<LOGG, H, C, true>(sm, tw, hi0, s0, P.q, P.two_q);
-        else ntt_rounds_fwd<LOGG, H, C, false>(sm, tw, hi0, s0, P.q, P.two_q);
-    } else {
-        ntt_rounds_inv<LOGG, H, C>(sm, tw, hi0, s0, P.q, P.two_q);
-    }
-
-    if (LAST) {
-#pragma unroll
-        for (int k = 0; k < NTT_EPT; k++) {
-            u64 v = sm[spad(t + k * T)];
-            if (FWD && lz) v = reduce64_lazy(v, P);
-            job.store(jc, j0 + k * jstep, v, P);
+    struct Env {
+        typename Job::Ctx jc;
+        PrimeConst P;
+        const ulonglong2* __restrict__ tw;
+        u32 t, hi0, lo0;
+        int log_n, s0, lo_bits;
+        u64 nq, four_q;
+        HS_DEV u32 gidx(u32 h, u32 g, u32 c) const {
+            return ((hi0 + h) << (log_n - s0)) | (g << lo_bits) | (lo0 + c);
         }
-    } else {
-        u64* __restrict__ dst = job.scratch(jc);
-#pragma unroll
-        for (int k = 0; k < NTT_EPT; k++) dst[j0 + k * jstep] = sm[spad(t + k * T)];
+    };
+
+    HS_DEV static u64 in(const Job& job, const Env& E, u32 j) {
+        if constexpr (FIRST) return job.load(E.jc, j, E.P);
+        else return job.scratch(E.jc)[j];
     }
+    template <bool LZ>
+    HS_DEV static void out(const Job& job, const Env& E, u32 j, u64 v) {
+        if constexpr (LAST) {
+            if (FWD && LZ) v = reduce64_lazy(v, E.P);
+            job.store(E.jc, j, v, E.P);
+        } else {
+            job.scratch(E.jc)[j] = v;
+        }
+    }
+
+    template <int r>
+    HS_DEV static void gather(const u64* buf, u64* v, const Env& E) {
+        using M = RM<r>;
+#pragma unroll
+        for (int k = 0; k < M::UPT; k++) {
+            const auto u = M::unit(E.t + k * T);
+            const u64* p = buf + spad16(u.base);
+#pragma unroll
+            for (int e = 0; e < M::NU; e++) v[k * M::NU + e] = p[M::off(e)];
+        }
+    }
+    template <int r>
+    HS_DEV static void scatter(u64* buf, const u64* v, const Env& E) {
+        using M = RM<r>;
+#pragma unroll
+        for (int k = 0; k < M::UPT; k++) {
+            const auto u = M::unit(E.t + k * T);
+            u64* p = buf + spad16(u.base);
+#pragma unroll
+            for (int e = 0; e < M::NU; e++) p[M::off(e)] = v[k * M::NU + e];
+        }
+    }
+    template <int r, bool LZ>
+    HS_DEV static void compute(u64* v, const Env& E) {
+        using M = RM<r>;
+#pragma unroll
+        for (int k = 0; k < M::UPT; k++) {
+            const auto u = M::unit(E.t + k * T);
+            const u32 Y = (((1u << E.s0) + E.hi0 + u.h) << M::AA) + u.gh;
+            unit_butterflies<FWD, LZ, M::RR>(v + k * M::NU, E.tw, Y, E.nq, E.P.two_q, E.four_q);
+        }
+    }
+
+    // rounds after the first, in execution order (I = 1 .. NR-1)
+    template <int I, bool LZ>
+    HS_DEV static void rest(u64* sm, u64* v, const Env& E) {
+        if constexpr (I < NR) {
+            constexpr int rp = FWD ? I - 1 : NR - I;        // previous round
+            constexpr int r = FWD ? I : NR - 1 - I;
+            u64* buf = sm + (I & 1) * SMW;
+            scatter<rp>(buf, v, E);
+            __syncthreads();
+            gather<r>(buf, v, E);
+            compute<r, LZ>(v, E);
+            rest<I + 1, LZ>(sm, v, E);
+        }
+    }
+
+    template <bool LZ>
+    HS_DEV static void run(u64* sm, const Env& E, const Job& job) {
+        u64 v[EPT];
+        using MF = RM<RFIRST>;
+        using ML = RM<RLAST>;
+        // ---- load
+        if constexpr (MF::direct) {
+            const u32 gstride = 1u << (MF::LOWB + E.lo_bits);
+#pragma unroll
+            for (int k = 0; k < MF::UPT; k++) {
+                const auto u = MF::unit(E.t + k * T);
+                const u32 j0 = E.gidx(u.h, u.g, u.c);
+#pragma unroll
+                for (int e = 0; e < MF::NU; e++) v[k * MF::NU + e] = in(job, E, j0 + e * gstride);
+            }
+        } else {
+            u64* buf = sm;                // "exchange 0": exchange I uses buffer I & 1
+#pragma unroll
+            for (int k = 0; k < EPT; k++) {
+                const u32 i = E.t + k * T;
+                buf[spad16(i)] = in(job, E, E.gidx(i / (G * C), (i / C) % G, i % C));
+            }
+            __syncthreads();
+            gather<RFIRST>(buf, v, E);
+        }
+        compute<RFIRST, LZ>(v, E);
+        rest<1, LZ>(sm, v, E);
+        // ---- store
+        if constexpr (ML::direct) {
+            const u32 gstride = 1u << (ML::LOWB + E.lo_bits);
+#pragma unroll
+            for (int k = 0; k < ML::UPT; k++) {
+                const auto u = ML::unit(E.t + k * T);
+                const u32 j0 = E.gidx(u.h, u.g, u.c);
+#pragma unroll
+                for (int e = 0; e < ML::NU; e++) out<LZ>(job, E, j0 + e * gstride, v[k * ML::NU + e]);
+            }
+        } else {
+            u64* buf = sm + (NR & 1) * SMW;   // the buffer not written by the last exchange
+            scatter<RLAST>(buf, v, E);
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < EPT; k++) {
+                const u32 i = E.t + k * T;
+                out<LZ>(job, E, E.gidx(i / (G * C), (i / C) % G, i % C), buf[spad16(i)]);
+            }
+        }
+    }
+};
+
+template <bool FWD, bool FIRST, bool LAST, int LOGG, int H, int C, int EPT, class Job>
+__global__ void __launch_bounds__(((H << LOGG) * C) / EPT)
+ntt_pass_kernel(Dev d, Job job, int s0, int jbase) {
+    using PE = PassEngine<FWD, FIRST, LAST, LOGG, H, C, EPT, Job>;
+    __shared__ u64 sm[2 * PE::SMW];
+    typename PE::Env E;
+    const int jb = jbase + (int)blockIdx.y;
+    E.jc = job.make(jb);
+    const int p = job.prime(E.jc);
+    E.P = d.pc[p];
+    E.tw = (FWD ? d.tw : d.itw) + (size_t)p * d.n;
+    E.log_n = d.log_n;
+    E.s0 = s0;
+    E.lo_bits = d.log_n - s0 - LOGG;
+    const u32 ncolblk = (1u << E.lo_bits) / C;
+    E.hi0 = (blockIdx.x / ncolblk) * H;
+    E.lo0 = (blockIdx.x % ncolblk) * C;
+    E.t = threadIdx.x;
+    E.nq = 0ull - E.P.q;
+    E.four_q = E.P.two_q << 1;
+    if (FWD && fwd_lazy_ok(E.P)) PE::template run<true>(sm, E, job);
+    else PE::template run<false>(sm, E, job);
 }
 
-// Single-pass variant for small limbs (whole limb in one CTA).
+// Single-pass variant for small limbs (whole limb in one CTA, 8 per thread).
 template <bool FWD, int LOGN, class Job>
 void launch_ntt_single(const Dev& d, const Job& job, int jbase, int njobs, cudaStream_t st) {
     dim3 grid(1, njobs);
-    const int threads = (1 << LOGN) / NTT_EPT;
-    ntt_pass_kernel<FWD, true, true, LOGN, 1, 1, Job><<<grid, threads, 0, st>>>(d, job, 0, jbase);
+    constexpr int EPT = LOGN >= 3 ? 8 : (1 << LOGN);
+    constexpr int threads = (1 << LOGN) / EPT;
+    ntt_pass_kernel<FWD, true, true, LOGN, 1, 1, EPT, Job><<<grid, threads, 0, st>>>(d, job, 0, jbase);
     note_launch();
 }
 
@@ -240,15 +438,16 @@ template <bool FWD, int LA, int LB, class Job>
 void launch_ntt_two(const Dev& d, const Job& job, int jbase, int njobs, cudaStream_t st) {
     constexpr int CA = NTT_TILE >> LA;   // columns per tile in pass A
     constexpr int HB = NTT_TILE >> LB;   // rows per tile in pass B
+    constexpr int TH = NTT_TILE / NTT_EPT16;
     const u32 n = 1u << (LA + LB);
     dim3 grid(n / NTT_TILE, njobs);
     note_launch(2);
     if constexpr (FWD) {
-        ntt_pass_kernel<true, true, false, LA, 1, CA, Job><<<grid, NTT_THREADS, 0, st>>>(d, job, 0, jbase);
-        ntt_pass_kernel<true, false, true, LB, HB, 1, Job><<<grid, NTT_THREADS, 0, st>>>(d, job, LA, jbase);
+        ntt_pass_kernel<true, true, false, LA, 1, CA, NTT_EPT16, Job><<<grid, TH, 0, st>>>(d, job, 0, jbase);
+        ntt_pass_kernel<true, false, true, LB, HB, 1, NTT_EPT16, Job><<<grid, TH, 0, st>>>(d, job, LA, jbase);
     } else {
-        ntt_pass_kernel<false, true, false, LB, HB, 1, Job><<<grid, NTT_THREADS, 0, st>>>(d, job, LA, jbase);
-        ntt_pass_kernel<false, false, true, LA, 1, CA, Job><<<grid, NTT_THREADS, 0, st>>>(d, job, 0, jbase);
+        ntt_pass_kernel<false, true, false, LB, HB, 1, NTT_EPT16, Job><<<grid, TH, 0, st>>>(d, job, LA, jbase);
+        ntt_pass_kernel<false, false, true, LA, 1, CA, NTT_EPT16, Job><<<grid, TH, 0, st>>>(d, job, 0, jbase);
     }
 }
 
