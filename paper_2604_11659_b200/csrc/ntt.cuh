@@ -56,7 +56,40 @@ HS_DEV u64 mulhi_apx(u64 x, u64 y) {
 // exact quotient estimate -> [0, 2q); approximate -> [0, 4q).
 // x*w - Q*q is formed as x*w + Q*(2^64 - q) (nq) so the chain is pure IMADs.
 HS_DEV u64 shoup_ex(u64 x, u64 w, u64 w_sh, u64 nq) { return x * w + mulhi_ex(x, w_sh) * nq; }
-HS_DEV u64 shoup_ax(u64 x, u64 w, u64 w_sh, u64 nq) { return x * w + mulhi_apx(x, w_sh) * nq; }
+
+// Approximate-quotient Shoup product in 11 integer instructions:
+//   Q = x1 s1 + hi(x1 s0) + hi(x0 s1)               (Q in [Q_exact - 2, Q_exact])
+//   r = lo64(x w + Q nq)                              (r in [0, 4q))
+HS_DEV u64 shoup_ax(u64 x, u64 w, u64 w_sh, u64 nq) {
+    u64 r;
+    asm("{\n\t"
+        ".reg .u32 x0, x1, w0, w1, s0, s1, n0, n1, a, b, q0, q1, t0, t1;\n\t"
+        ".reg .u64 Q, T;\n\t"
+        "mov.b64 {x0, x1}, %1;\n\t"
+        "mov.b64 {w0, w1}, %2;\n\t"
+        "mov.b64 {s0, s1}, %3;\n\t"
+        "mov.b64 {n0, n1}, %4;\n\t"
+        "mul.hi.u32 a, x1, s0;\n\t"
+        "mul.hi.u32 b, x0, s1;\n\t"
+        "mul.wide.u32 Q, x1, s1;\n\t"
+        "mov.b64 {q0, q1}, Q;\n\t"
+        "add.cc.u32 q0, q0, a;\n\t"
+        "addc.u32 q1, q1, 0;\n\t"
+        "add.cc.u32 q0, q0, b;\n\t"
+        "addc.u32 q1, q1, 0;\n\t"
+        "mul.wide.u32 T, x0, w0;\n\t"
+        "mad.wide.u32 T, q0, n0, T;\n\t"
+        "mov.b64 {t0, t1}, T;\n\t"
+        "mad.lo.u32 t1, x0, w1, t1;\n\t"
+        "mad.lo.u32 t1, x1, w0, t1;\n\t"
+        "mad.lo.u32 t1, q0, n1, t1;\n\t"
+        "mad.lo.u32 t1, q1, n0, t1;\n\t"
+        "mov.b64 %0, {t0, t1};\n\t"
+        "}"
+        : "=l"(r)
+        : "l"(x), "l"(w), "l"(w_sh), "l"(nq));
+    return r;
+}
 
 // Forward passes run fully lazy ("LZ") when every intermediate stays far
 // below 2^63: inputs < 4q, each of <= 17 stages adds < 4q (approximate Shoup),
@@ -236,20 +269,16 @@ HS_DEV void unit_butterflies(u64* v, const ulonglong2* __restrict__ tw, u32 Y, u
         for (int e = 0; e < NU; e++) {
             if (e & bit) continue;
             const ulonglong2 w = twp[e >> (R - j)];
-            if (FWD && LZ) {
-                const u64 x = v[e];
+            if (FWD) {
+                // LZ: x unbounded-lazy (grows < 4q per stage); else [0, 8q) -> [0, 4q)
+                const u64 x = LZ ? v[e] : csub_s(v[e], four_q);
                 const u64 t = shoup_ax(v[e + bit], w.x, w.y, nq);          // [0, 4q)
                 v[e] = x + t;
                 v[e + bit] = x - t + four_q;
-            } else if (FWD) {
-                const u64 x = csub_s(v[e], two_q);                        // [0, 2q)
-                const u64 t = shoup_ex(v[e + bit], w.x, w.y, nq);          // [0, 2q)
-                v[e] = x + t;
-                v[e + bit] = x - t + two_q;
             } else {
-                const u64 x = v[e], y = v[e + bit];                      // [0, 2q)
-                v[e] = csub_s(x + y, two_q);
-                v[e + bit] = shoup_ex(x - y + two_q, w.x, w.y, nq);
+                const u64 x = v[e], y = v[e + bit];                      // [0, 4q)
+                v[e] = csub_s(x + y, four_q);
+                v[e + bit] = shoup_ax(x - y + four_q, w.x, w.y, nq);       // [0, 4q)
             }
         }
     }
@@ -259,7 +288,9 @@ HS_DEV void unit_butterflies(u64* v, const ulonglong2* __restrict__ tw, u32 Y, u
 // CTA (pointer-table lookups, index decoding), then prime(ctx),
 // load(ctx, j, P), scratch(ctx), store(ctx, j, v, P) per element.  load()
 // returns [0, q) (forward loads may return up to 4q); store() receives
-// [0, 4q) forward and [0, 2q) inverse.
+// [0, 4q) in both directions.  Internal invariants: forward LZ values grow
+// by < 4q per stage from < 4q; forward Harvey values stay in [0, 8q) (csub
+// by 4q, approximate Shoup in [0, 4q)); inverse values stay in [0, 4q).
 template <bool FWD, bool FIRST, bool LAST, int LOGG, int H, int C, int EPT, class Job>
 struct PassEngine {
     using PL = Plan<LOGG, EPT>;
@@ -292,7 +323,7 @@ struct PassEngine {
     template <bool LZ>
     HS_DEV static void out(const Job& job, const Env& E, u32 j, u64 v) {
         if constexpr (LAST) {
-            if (FWD && LZ) v = reduce64_lazy(v, E.P);
+            if (FWD) v = LZ ? reduce64_lazy(v, E.P) : csub_s(v, E.four_q);
             job.store(E.jc, j, v, E.P);
         } else {
             job.scratch(E.jc)[j] = v;

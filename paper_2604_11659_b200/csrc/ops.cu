@@ -409,13 +409,10 @@ modup_inner_kernel(Dev d, int l, const u64* __restrict__ E, const u64* const* __
 #pragma unroll
             for (int k = 0; k < NTT_EPT; k++) ext[k] = src[t + k * NTT_THREADS];
         } else {
-            // pass A ran lazily for small primes (ntt.cuh): back to [0, 2q)
-            const bool lz = fwd_lazy_ok(P);
+            // pass A leaves lazy values (ntt.cuh invariants): back to [0, 4q)
 #pragma unroll
-            for (int k = 0; k < NTT_EPT; k++) {
-                const u64 v = src[t + k * NTT_THREADS];
-                sm[spad(t + k * NTT_THREADS)] = lz ? reduce64_lazy(v, P) : v;
-            }
+            for (int k = 0; k < NTT_EPT; k++)
+                sm[spad(t + k * NTT_THREADS)] = reduce64_lazy(src[t + k * NTT_THREADS], P);
             __syncthreads();
             ntt_rounds_fwd<LB, H, 1>(sm, tw, hi0, LA, P.q, P.two_q);
 #pragma unroll
