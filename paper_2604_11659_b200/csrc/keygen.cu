@@ -412,6 +412,7 @@ struct ParArgs {
     unsigned* fastb;       // [K][W/32]
     unsigned* emitb;       // [K][W/32]
     double* tailx;         // [K][W] values of tail tokens (sparse)
+    u32* tlen;             // [K][W] draws consumed by a tail token (sparse, 0 = window too short)
     u64* pos_in;           // [K] segment start
     u64* pos_out;          // [K] next segment start
     u64* const* a_out;     // [K] a half of each key
@@ -514,87 +515,246 @@ __global__ void __launch_bounds__(RNG_T) pk_uniform_write(ParArgs A, int digit, 
     }
 }
 
-// Normal segment token walk (one warp per key) -> emit bitmap, tail values,
-// per-tile emit counts (exclusive prefix) and the next segment start.
-__global__ void pk_normal_walk(ParArgs A) {
+// Normal segment token parse, one CTA per key, everything in shared memory:
+//  1. every non-fast position s is evaluated as if it started a token:
+//     layer zs != 0 -> accept bit from the exp test with draw s+1 (2 draws);
+//     zs == 0 (tail) -> value and length 1 + 2k of the log1p loop;
+//  2. warp 0 walks the token chain: 32 bitmap words per ballot to find the
+//     next slow position, counting the fast tokens in between; only slow
+//     token starts are visited one by one (about 1 in 80 positions);
+//  3. emit bits = (fast & not consumed) | accepted slow starts, up to the
+//     n-th emission; per-tile exclusive prefix counts for pk_normal_write.
+constexpr int NW_T = 512;
+
+// Clear bits [lo, hi) of a shared bitmap (one warp).
+HS_DEV void clear_bits(unsigned* bmp, u32 lo, u32 hi, u32 lane) {
+    if (lo >= hi) return;
+    for (u32 w = (lo >> 5) + lane; w <= ((hi - 1) >> 5); w += 32) {
+        const u32 b0 = max(lo, w << 5) - (w << 5), b1 = min(hi, (w + 1) << 5) - (w << 5);
+        const unsigned m = (b1 - b0 == 32u) ? 0xffffffffu : (((1u << (b1 - b0)) - 1u) << b0);
+        bmp[w] &= ~m;
+    }
+}
+
+// Walk the token chain from token start c while c < stop (one warp): fast
+// positions are single-draw tokens; a slow position s starts a token of 2
+// draws (tail: tl[s]).  Marks slow starts in sb and consumed draws in cb;
+// returns the first token start >= stop.  A token running past the window
+// sets trunc to its start and ends the walk (returns W).
+HS_DEV u32 walk_chain(u32 c, u32 stop, const unsigned* fb, const unsigned* tb, unsigned* sb,
+                      unsigned* cb, const u32* tl, u32 W, u32 lane, u32& trunc) {
+    while (c < stop) {
+        const u32 w0 = c >> 5;
+        const u32 w = w0 + lane;
+        unsigned x = 0u;
+        if ((w << 5) < stop) {
+            x = ~fb[w];
+            if (lane == 0) x &= ~((1u << (c & 31)) - 1u);
+            const u32 top = stop - (w << 5);
+            if (top < 32u) x &= (1u << top) - 1u;
+        }
+        const unsigned ball = __ballot_sync(0xffffffffu, x != 0u);
+        if (ball == 0u) {
+            c = min((w0 + 32u) << 5, stop);
+            continue;
+        }
+        const int f = __ffs(ball) - 1;
+        const unsigned xf = __shfl_sync(0xffffffffu, x, f);
+        const u32 s = ((w0 + (u32)f) << 5) + (u32)(__ffs(xf) - 1);
+        const unsigned bit = 1u << (s & 31);
+        const u32 len = (tb[s >> 5] & bit) ? tl[s] : 2u;
+        if (len == 0 || s + len > W) {       // token runs past the window: chain truncated at s
+            trunc = s;
+            return W;
+        }
+        if (lane == 0) {            // neighbouring pieces may share a word: atomics
+            atomicOr(&sb[s >> 5], bit);
+            for (u32 p = s + 1; p < s + len; p++) atomicOr(&cb[p >> 5], 1u << (p & 31));
+        }
+        __syncwarp();
+        c = s + len;
+    }
+    return c;
+}
+
+__global__ void __launch_bounds__(NW_T) pk_normal_walk2(ParArgs A) {
+    extern __shared__ unsigned bm[];
     const int k = blockIdx.x;
-    const u32 lane = threadIdx.x;
-    const u32 n = A.n;
     const int words = A.W / 32;
-    const unsigned* fb = A.fastb + (size_t)k * words;
-    unsigned* eb = A.emitb + (size_t)k * words;
+    unsigned* fb = bm;                 // fast-path bits
+    unsigned* ab = bm + words;         // slow token would emit (layer test / tail)
+    unsigned* tb = bm + 2 * words;     // slow token is a tail
+    unsigned* cb = bm + 3 * words;     // consumed as a uniform by a token start
+    unsigned* sb = bm + 4 * words;     // slow token starts
+    __shared__ int s_err;
+    __shared__ u32 s_tile[64];
+    const u32 t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const u32 n = A.n;
+    const u32 W = (u32)A.W;
+    const unsigned* gfb = A.fastb + (size_t)k * words;
     const u64* raw = A.raw + (size_t)k * A.W;
     double* tx = A.tailx + (size_t)k * A.W;
-    for (int w = lane; w < words; w += 32) eb[w] = 0u;
-    __syncwarp();
-    if (lane == 0) {
-        u32 c = 0, cntv = 0;
-        bool done = false;
-        while (!done && c < (u32)A.W) {
-            // next non-fast position >= c
-            u32 s = (u32)A.W;
-            for (u32 w = c >> 5; w < (u32)words; w++) {
-                unsigned bits = ~fb[w];
-                if (w == (c >> 5)) bits &= ~((1u << (c & 31)) - 1u);
-                if (bits) {
-                    s = (w << 5) + __ffs(bits) - 1;
-                    break;
-                }
-            }
-            u32 run = s - c;
-            if (cntv + run >= n) {
-                run = n - cntv;
-                done = true;
-            }
-            set_bit_range(eb, c, c + run);
-            cntv += run;
-            c += run;
-            if (done || s >= (u32)A.W) break;
+    u32* tl = A.tlen + (size_t)k * A.W;
+    for (int w = t; w < words; w += NW_T) {
+        fb[w] = gfb[w];
+        cb[w] = 0u;
+        sb[w] = 0u;
+    }
+    if (t == 0) s_err = 0;
+    __syncthreads();
+    // ---- 1. speculative evaluation of every slow position
+    for (int w = t; w < words; w += NW_T) {
+        unsigned slow = ~fb[w], acc = 0u, tail = 0u;
+        while (slow) {
+            const int b = __ffs(slow) - 1;
+            slow &= slow - 1u;
+            const u32 s = (u32)w * 32u + (u32)b;
             const u64 rs = raw[s];
             const int zs = (int)(rs & 0xff);
             const u64 rabs = ((rs >> 8) >> 1) & 0x000fffffffffffffull;
-            if (s + 2 >= (u32)A.W) break;                   // window exhausted
             if (zs != 0) {
+                if (s + 1 >= W) continue;                     // cannot be decided: walk errors out
                 double xs = (double)rabs * A.zig->wi[zs];
                 if ((rs >> 8) & 1) xs = -xs;
                 const double u = next_double_of(raw[s + 1]);
-                if ((A.zig->fi[zs - 1] - A.zig->fi[zs]) * u + A.zig->fi[zs] < exp(-0.5 * xs * xs)) {
-                    eb[s >> 5] |= 1u << (s & 31);
-                    if (++cntv >= n) done = true;
-                }
-                c = s + 2;
+                if ((A.zig->fi[zs - 1] - A.zig->fi[zs]) * u + A.zig->fi[zs] < exp(-0.5 * xs * xs))
+                    acc |= 1u << b;
             } else {
-                u32 pos = s + 1;
-                double v = 0.0;
-                bool ok = false;
-                while (pos + 1 < (u32)A.W) {
+                tail |= 1u << b;
+                acc |= 1u << b;
+                u32 pos = s + 1, len = 0;
+                while (pos + 1 < W) {
                     const double xx = -ZIG_INV_R * log1p(-next_double_of(raw[pos]));
                     const double yy = -log1p(-next_double_of(raw[pos + 1]));
                     pos += 2;
                     if (yy + yy > xx * xx) {
-                        v = ((rabs >> 8) & 1) ? -(ZIG_R + xx) : ZIG_R + xx;
-                        ok = true;
+                        tx[s] = ((rabs >> 8) & 1) ? -(ZIG_R + xx) : ZIG_R + xx;
+                        len = pos - s;
                         break;
                     }
                 }
-                if (!ok) break;
-                tx[s] = v;
-                eb[s >> 5] |= 1u << (s & 31);
-                if (++cntv >= n) done = true;
-                c = pos;
+                tl[s] = len;
             }
         }
-        if (!done) *A.err = 1;
-        A.pos_out[k] = A.pos_in[k] + c;
+        ab[w] = acc;
+        tb[w] = tail;
     }
-    __syncwarp();
-    // exclusive per-tile prefix of emits (tiles of RNG_CH positions)
-    if (lane == 0) {
-        u32 run = 0;
-        for (int tile = 0; tile < A.NT; tile++) {
-            A.cnt[(size_t)k * A.NT + tile] = run;
-            for (int w = tile * (RNG_CH / 32); w < (tile + 1) * (RNG_CH / 32); w++) run += __popc(eb[w]);
+    __syncthreads();
+    // ---- 2. token chain: speculative walks of 16 pieces, then serial fix-ups
+    // (a piece's entry is its first position unless the previous piece's last
+    // token spills over it; chains re-synchronise within a token or two).
+    // A token running past the window end truncates the chain there; the
+    // segment is valid only if its n-th emission comes before that point.
+    constexpr int NWARP = NW_T / 32;
+    __shared__ u32 s_exit[NWARP], s_trunc[NWARP];
+    __shared__ u32 s_chain_trunc;
+    const u32 pw = ((u32)words + NWARP - 1) / NWARP;          // words per piece
+    {
+        const u32 ps = min(warp * pw, (u32)words) << 5, pe = min((warp + 1) * pw, (u32)words) << 5;
+        u32 tr = W;
+        const u32 x = walk_chain(ps, pe, fb, tb, sb, cb, tl, W, lane, tr);
+        if (lane == 0) {
+            s_exit[warp] = x;
+            s_trunc[warp] = tr;
         }
+    }
+    __syncthreads();
+    if (warp == 0) {
+        u32 actual = s_exit[0], ctr = s_trunc[0];
+        bool dirty = false;                  // a re-walk cleared marks inside piece i
+        for (int i = 1; i < NWARP && ctr == W; i++) {
+            const u32 ps = min((u32)i * pw, (u32)words) << 5, pe = min((u32)(i + 1) * pw, (u32)words) << 5;
+            if (ps >= pe) continue;
+            if (actual == ps && !dirty) {
+                actual = s_exit[i];
+                ctr = s_trunc[i];
+                continue;
+            }
+            // misprediction: drop piece i's speculative marks, re-walk from `actual`
+            const u32 spec_end = max(s_exit[i], actual);
+            clear_bits(sb, ps, spec_end, lane);
+            clear_bits(cb, actual, spec_end, lane);
+            __syncwarp();
+            actual = walk_chain(actual, pe, fb, tb, sb, cb, tl, W, lane, ctr);
+            dirty = spec_end > pe;
+        }
+        if (lane == 0) s_chain_trunc = ctr;
+    }
+    __syncthreads();
+    // ---- 3. emissions = (fast & not consumed) | emitting slow starts; the
+    // segment ends after the n-th emission
+    constexpr int WPTH = 12;                                // words per thread in the scan (W <= 196608)
+    __shared__ u32 s_wsum[NW_T / 32];
+    __shared__ u32 s_pos;
+    u32 pop[WPTH], tsum = 0;
+#pragma unroll
+    for (int q = 0; q < WPTH; q++) {
+        const u32 w = t * WPTH + q;
+        pop[q] = w < (u32)words ? __popc((fb[w] & ~cb[w]) | (ab[w] & sb[w])) : 0u;
+        tsum += pop[q];
+    }
+    u32 inc = tsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u32 v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= (u32)o) inc += v;
+    }
+    if (lane == 31) s_wsum[warp] = inc;
+    if (t == 0) s_pos = 0xffffffffu;
+    __syncthreads();
+    u32 before = inc - tsum;
+    for (int w = 0; w < (int)warp; w++) before += s_wsum[w];
+    if (!s_err && before < n && before + tsum >= n) {
+        u32 need = n - before;                              // 1-based rank within this thread's words
+#pragma unroll
+        for (int q = 0; q < WPTH; q++) {
+            if (need > pop[q]) {
+                need -= pop[q];
+                continue;
+            }
+            const u32 w = t * WPTH + q;
+            unsigned e = (fb[w] & ~cb[w]) | (ab[w] & sb[w]);
+            for (u32 r = 1; r < need; r++) e &= e - 1u;
+            s_pos = (w << 5) + (u32)(__ffs(e) - 1);
+            break;
+        }
+    }
+    __syncthreads();
+    if (s_err || s_pos >= s_chain_trunc) {
+        if (t == 0) {
+            *A.err = 1;
+            A.pos_out[k] = A.pos_in[k];
+        }
+        return;
+    }
+    const u32 last = s_pos;                                 // position of the n-th emission
+    const unsigned lbit = 1u << (last & 31);
+    const u32 end = (sb[last >> 5] & lbit) ? last + ((tb[last >> 5] & lbit) ? tl[last] : 2u) : last + 1u;
+    unsigned* eb = A.emitb + (size_t)k * words;
+    constexpr int WPT = RNG_CH / 32;       // words per tile
+    const int NT = A.NT;
+    for (int tile = warp; tile < NT; tile += NW_T / 32) {
+        u32 sum = 0;
+        for (int w = tile * WPT + lane; w < (tile + 1) * WPT; w += 32) {
+            unsigned e = (fb[w] & ~cb[w]) | (ab[w] & sb[w]);
+            const u32 base = (u32)w << 5;
+            if (base > last) e = 0u;
+            else if (last - base < 31u) e &= (2u << (last - base)) - 1u;
+            eb[w] = e;
+            sum += __popc(e);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (lane == 0) s_tile[tile] = sum;
+    }
+    __syncthreads();
+    if (t == 0) {
+        u32 run = 0;
+        for (int tile = 0; tile < NT; tile++) {
+            A.cnt[(size_t)k * NT + tile] = run;
+            run += s_tile[tile];
+        }
+        A.pos_out[k] = A.pos_in[k] + end;
     }
 }
 
@@ -647,7 +807,7 @@ size_t keygen_par_window(u32 n) {
 
 size_t keygen_par_scratch_bytes(int K, u32 n) {
     const size_t W = keygen_par_window(n), NT = W / RNG_CH;
-    return (size_t)K * (W * 8 + W * 8 + W / 32 * 4 * 2 + NT * 4) + (size_t)K * 16 + 64;
+    return (size_t)K * (W * 8 + W * 8 + W * 4 + W / 32 * 4 * 2 + NT * 4) + (size_t)K * 16 + 64;
 }
 
 // Replays K key streams in lockstep.  Returns false (nothing guaranteed) if
@@ -667,6 +827,8 @@ void keygen_streams_parallel(const Dev& d, int K, const void* streams, u64* cons
     p += (size_t)K * W * 8;
     A.tailx = (double*)p;
     p += (size_t)K * W * 8;
+    A.tlen = (u32*)p;
+    p += (size_t)K * W * 4;
     A.fastb = (unsigned*)p;
     p += (size_t)K * (W / 32) * 4;
     A.emitb = (unsigned*)p;
@@ -685,6 +847,8 @@ void keygen_streams_parallel(const Dev& d, int K, const void* streams, u64* cons
     A.n = d.n;
     int cur = 0;
     const dim3 grid(NT, K);
+    const size_t walk_smem = (size_t)5 * (W / 32) * sizeof(unsigned);
+    cudaFuncSetAttribute(pk_normal_walk2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)walk_smem);
     for (int digit = 0; digit <= d.L; digit++) {
         for (int m = 0; m < d.L + 2; m++) {
             A.pos_in = pos[cur];
@@ -697,7 +861,7 @@ void keygen_streams_parallel(const Dev& d, int K, const void* streams, u64* cons
         A.pos_in = pos[cur];
         A.pos_out = pos[cur ^ 1];
         pk_gen_kernel<<<grid, RNG_T, 0, st>>>(A, 1, 0);
-        pk_normal_walk<<<K, 32, 0, st>>>(A);
+        pk_normal_walk2<<<K, NW_T, walk_smem, st>>>(A);
         pk_normal_write<<<grid, RNG_T, 0, st>>>(A, digit);
         note_launch(3);
         cur ^= 1;
@@ -805,9 +969,25 @@ struct JobKeyFused {
             const u32 pj = __brev((ex - 1) >> 1) >> (32 - d.log_n);
             acc = add_mod(acc, shoup(c.skm[pj], c.f.x, c.f.y, P.q), P.q);
         }
-        c.b[j] = sub_mod(acc, mul_mod(c.a[j], c.skm[j], P), P.q);
+        // a * sk with sk's Shoup companion (stored after the L+2 sk limbs)
+        const u64 ask = csub(shoup_lazy(c.a[j], c.skm[j], c.skm[(size_t)(L + 2) * d.n + j], P.q), P.q);
+        c.b[j] = sub_mod(acc, ask, P.q);
     }
 };
+
+__global__ void shoup_companion_kernel(Dev d, const u64* v, u64* sh) {
+    const u32 j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= d.n) return;
+    const int m = blockIdx.y;
+    const size_t o = (size_t)m * d.n + j;
+    sh[o] = (u64)(((unsigned __int128)v[o] << 64) / d.pc[m].q);
+}
+
+// sh[m][j] = floor(v[m][j] 2^64 / q_m) for nl limbs of moduli 0..nl-1.
+void shoup_companions(const Dev& d, const u64* v, u64* sh, int nl, cudaStream_t st) {
+    shoup_companion_kernel<<<dim3((d.n + 255) / 256, nl), 256, 0, st>>>(d, v, sh);
+    note_launch();
+}
 
 void keygen_assemble(const Dev& d, int K, u64* const* keys, const long long* e, const u32* gal,
                      const u64* sk, const ulonglong2* f, cudaStream_t st) {
@@ -993,8 +1173,9 @@ hs_status hs_keygen_set_tables(hs_ctx* c, const double* wi, const double* fi, co
 
 hs_status hs_keygen_set_secret(hs_ctx* c, const uint64_t* sk_ntt, void* stream) {
     const size_t bytes = (size_t)(c->L + 2) * c->n * sizeof(u64);
-    if (!c->d_sk) HS_CUDA(cudaMalloc((void**)&c->d_sk, bytes));
+    if (!c->d_sk) HS_CUDA(cudaMalloc((void**)&c->d_sk, 2 * bytes));     // values, then Shoup companions
     HS_CUDA(cudaMemcpyAsync(c->d_sk, sk_ntt, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    shoup_companions(c->dev, c->d_sk, c->d_sk + (size_t)(c->L + 2) * c->n, c->L + 2, (cudaStream_t)stream);
     return HS_OK;
 }
 
@@ -1061,7 +1242,23 @@ hs_status hs_keygen_streams(hs_ctx* c, const uint64_t* states, int32_t nkeys, ui
     HS_CUDA(cudaMallocAsync(&d_streams, nkeys * 4 * sizeof(u64), st));
     HS_CUDA(cudaMemcpyAsync(d_aout, aout.data(), nkeys * sizeof(u64*), cudaMemcpyHostToDevice, st));
     HS_CUDA(cudaMemcpyAsync(d_streams, states, nkeys * 4 * sizeof(u64), cudaMemcpyHostToDevice, st));
-    keygen_streams(c->dev, nkeys, d_streams, d_aout, (long long*)e_out, c->d_jump, c->d_zig, c->d_thr, st);
+    // the production (grid-parallel) path; the serial replay if a window overflowed
+    if (!c->d_kg_err) {
+        HS_CUDA(cudaMalloc((void**)&c->d_kg_err, sizeof(int)));
+        HS_CUDA(cudaMemset(c->d_kg_err, 0, sizeof(int)));
+    }
+    void* scratch = nullptr;
+    HS_CUDA(cudaMallocAsync(&scratch, keygen_par_scratch_bytes(nkeys, c->n), st));
+    keygen_streams_parallel(c->dev, nkeys, d_streams, d_aout, (long long*)e_out, c->d_jump, c->d_zig,
+                            c->d_thr, scratch, c->d_kg_err, st);
+    HS_CUDA(cudaStreamSynchronize(st));
+    cudaFreeAsync(scratch, st);
+    int err = 0;
+    HS_CUDA(cudaMemcpy(&err, c->d_kg_err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (err) {
+        HS_CUDA(cudaMemset(c->d_kg_err, 0, sizeof(int)));
+        keygen_streams(c->dev, nkeys, d_streams, d_aout, (long long*)e_out, c->d_jump, c->d_zig, c->d_thr, st);
+    }
     HS_CUDA(cudaStreamSynchronize(st));
     cudaFreeAsync(d_aout, st);
     cudaFreeAsync(d_streams, st);

@@ -87,6 +87,7 @@ size_t keygen_par_scratch_bytes(int K, u32 n);
 void keygen_streams_parallel(const Dev& d, int K, const void* streams, u64* const* a_out,
                              long long* e_out, const void* jump, const void* zig, const u64* thr,
                              void* scratch, int* err, cudaStream_t st);
+void shoup_companions(const Dev& d, const u64* v, u64* sh, int nl, cudaStream_t st);
 void keygen_assemble(const Dev& d, int K, u64* const* keys, const long long* e, const u32* gal,
                      const u64* sk, const ulonglong2* f, cudaStream_t st);
 

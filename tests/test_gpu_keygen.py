@@ -34,8 +34,9 @@ def _numpy_draws(params, seed, r):
     return a, e
 
 
-@pytest.mark.parametrize("n,sb,L", [(64, 40, 2), (1024, 45, 2), (16384, 50, 2), (8192, 40, 4)])
-def test_device_stream_replays_numpy(pkg, n, sb, L):
+@pytest.mark.parametrize("n,sb,L,nkeys", [(64, 40, 2, 5), (1024, 45, 2, 5), (16384, 50, 2, 5), (8192, 40, 4, 5),
+                                          (4096, 50, 6, 24)])
+def test_device_stream_replays_numpy(pkg, n, sb, L, nkeys):
     from paper_2604_11659_b200 import device as D
     from paper_2604_11659_b200._lib import check, lib
     from paper_2604_11659_b200.rng import galois_states, ziggurat_tables
@@ -45,7 +46,7 @@ def test_device_stream_replays_numpy(pkg, n, sb, L):
     check(lib().hs_keygen_set_tables(ctx.handle, wi.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
                                      fi.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
                                      ki.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))))
-    steps = [1, 3, n // 2 - 1, 7, 11]
+    steps = ([1, 3, n // 2 - 1, 7, 11] + list(range(13, 13 + 2 * nkeys, 2)))[:nkeys]
     st = np.ascontiguousarray(galois_states(2024, steps))
     K = len(steps)
     a = D.empty((K, L + 1, L + 2, n))
