@@ -426,11 +426,31 @@ struct ParArgs {
 // the key's start state by P (power-of-two compositions), threads fan out.
 HS_DEV U128 tile_state(const ParArgs& A, const KeyStream& ks, u64 P, U128* s_x) {
     const U128 inc{ks.inc_hi, ks.inc_lo};
-    if (threadIdx.x == 0) {
-        U128 x{ks.state_hi, ks.state_lo};
-        for (int j = 0; P; j++, P >>= 1)
-            if (P & 1) x = add128(mul128(A.jump->PA[j], x), mul128(A.jump->PS[j], inc));
-        *s_x = x;
+    if (threadIdx.x < 32) {
+        // jumps by 2^j commute: lane l composes the set bits l and l+32 of P,
+        // then a butterfly reduction composes the 32 affine maps x -> Ax + B
+        const u32 l = threadIdx.x;
+        U128 Am{0, 1}, Bm{0, 0};
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const u32 j = l + 32u * h;
+            if ((P >> j) & 1ull) {
+                const U128 Aj = A.jump->PA[j], Bj = mul128(A.jump->PS[j], inc);
+                Bm = add128(mul128(Aj, Bm), Bj);
+                Am = mul128(Aj, Am);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            U128 Ao, Bo;
+            Ao.hi = __shfl_xor_sync(0xffffffffu, Am.hi, o);
+            Ao.lo = __shfl_xor_sync(0xffffffffu, Am.lo, o);
+            Bo.hi = __shfl_xor_sync(0xffffffffu, Bm.hi, o);
+            Bo.lo = __shfl_xor_sync(0xffffffffu, Bm.lo, o);
+            Bm = add128(mul128(Ao, Bm), Bo);
+            Am = mul128(Ao, Am);
+        }
+        if (l == 0) *s_x = add128(mul128(Am, U128{ks.state_hi, ks.state_lo}), Bm);
     }
     __syncthreads();
     const U128 x = *s_x;
@@ -478,42 +498,89 @@ __global__ void __launch_bounds__(RNG_T) pk_gen_kernel(ParArgs A, int normal, in
     }
 }
 
-// Uniform segment: write the first n accepted values in stream order.
-__global__ void __launch_bounds__(RNG_T) pk_uniform_write(ParArgs A, int digit, int sidx) {
+// Uniform segment in one launch (decoupled look-back): each tile generates
+// its draws, publishes its Lemire accept count (tagged with the launch
+// sequence number), sums its predecessors' counts and writes its accepted
+// values at their stream ranks.  Tiles that may lie past the segment end
+// look back first and skip generation when the segment is already complete.
+HS_DEV void publish(unsigned long long* f, u32 seq, u32 v) {
+    const unsigned long long x = ((unsigned long long)seq << 32) | v;
+    // the flag word carries the count itself: relaxed ordering suffices
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(f), "l"(x) : "memory");
+}
+HS_DEV u32 look_back(const unsigned long long* fl, int tile, u32 seq) {
+    u32 sum = 0;
+    for (int j = (int)(threadIdx.x & 31); j < tile; j += 32) {
+        unsigned long long x;
+        do {
+            asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(x) : "l"(fl + j) : "memory");
+        } while ((u32)(x >> 32) != seq);
+        sum += (u32)x;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    return sum;
+}
+
+__global__ void __launch_bounds__(RNG_T) pk_uniform_fused(ParArgs A, int digit, int sidx,
+                                                          unsigned long long* flags, u32 seq) {
+    __shared__ U128 s_x;
     __shared__ u32 cnt[RNG_E * RNG_W];
     __shared__ u32 s_total, s_prefix;
     const int k = blockIdx.y, tile = blockIdx.x;
     const u32 t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const unsigned lt = (1u << lane) - 1u;
     const u32 n = A.n;
-    if (t == 0) {
-        u32 p = 0;
-        for (int j = 0; j < tile; j++) p += A.cnt[(size_t)k * A.NT + j];
-        s_prefix = p;
-        if (tile == A.NT - 1 && p + A.cnt[(size_t)k * A.NT + tile] < n) *A.err = 1;
+    unsigned long long* fl = flags + (size_t)k * A.NT;
+    const bool spec = (u64)tile * RNG_CH >= n;
+    if (spec) {
+        if (warp == 0) {
+            const u32 p = look_back(fl, tile, seq);
+            if (lane == 0) s_prefix = p;
+        }
+        __syncthreads();
+        if (s_prefix >= n) {
+            if (t == 0) publish(fl + tile, seq, 0u);
+            return;
+        }
     }
-    __syncthreads();
-    const u32 prefix = s_prefix;
-    if (prefix >= n) return;
+    const KeyStream ks = A.streams[k];
+    const U128 inc{ks.inc_hi, ks.inc_lo};
+    U128 s = tile_state(A, ks, A.pos_in[k] + (u64)tile * RNG_CH, &s_x);
+    const U128 AT = A.jump->A[RNG_T], CT = mul128(A.jump->S[RNG_T], inc);
     const u64 q = A.pc[sidx].q, thr = A.thr[sidx];
-    const u64* raw = A.raw + (size_t)k * A.W + (size_t)tile * RNG_CH;
+    u64 val[RNG_E];
     unsigned ball[RNG_E];
 #pragma unroll
     for (int e = 0; e < RNG_E; e++) {
-        ball[e] = __ballot_sync(0xffffffffu, raw[e * RNG_T + t] * q >= thr);
+        const u64 x = xsl_rr(s);
+        s = add128(mul128(s, AT), CT);
+        val[e] = __umul64hi(x, q);
+        ball[e] = __ballot_sync(0xffffffffu, x * q >= thr);
         if (lane == 0) cnt[e * RNG_W + warp] = __popc(ball[e]);
     }
-    chunk_scan(cnt, &s_total);
+    const u32 total = chunk_scan(cnt, &s_total);
+    if (t == 0) publish(fl + tile, seq, total);
+    if (!spec) {
+        if (warp == 0) {
+            const u32 p = look_back(fl, tile, seq);
+            if (lane == 0) s_prefix = p;
+        }
+        __syncthreads();
+    }
+    const u32 prefix = s_prefix;
+    if (t == 0 && tile == A.NT - 1 && prefix + total < n) *A.err = 1;
+    if (prefix >= n) return;
     u64* dst = A.a_out[k] + ((size_t)digit * (A.L + 2) + sidx) * n;
 #pragma unroll
     for (int e = 0; e < RNG_E; e++) {
         if (!((ball[e] >> lane) & 1u)) continue;
         const u32 idx = prefix + cnt[e * RNG_W + warp] + __popc(ball[e] & lt);
-        const u32 i = e * RNG_T + t;
-        if (idx < n) dst[idx] = __umul64hi(raw[i], q);
-        if (idx == n - 1) A.pos_out[k] = A.pos_in[k] + (u64)tile * RNG_CH + i + 1;
+        if (idx < n) dst[idx] = val[e];
+        if (idx == n - 1) A.pos_out[k] = A.pos_in[k] + (u64)tile * RNG_CH + e * RNG_T + t + 1;
     }
 }
+
 
 // Normal segment token parse, one CTA per key, everything in shared memory:
 //  1. every non-fast position s is evaluated as if it started a token:
@@ -807,7 +874,7 @@ size_t keygen_par_window(u32 n) {
 
 size_t keygen_par_scratch_bytes(int K, u32 n) {
     const size_t W = keygen_par_window(n), NT = W / RNG_CH;
-    return (size_t)K * (W * 8 + W * 8 + W * 4 + W / 32 * 4 * 2 + NT * 4) + (size_t)K * 16 + 64;
+    return (size_t)K * (W * 8 + W * 8 + W * 4 + W / 32 * 4 * 2 + NT * 4 + NT * 8) + (size_t)K * 16 + 128;
 }
 
 // Replays K key streams in lockstep.  Returns false (nothing guaranteed) if
@@ -837,6 +904,10 @@ void keygen_streams_parallel(const Dev& d, int K, const void* streams, u64* cons
     p += (size_t)K * NT * 4;
     p = (char*)(((uintptr_t)p + 15) & ~(uintptr_t)15);     // K * NT may be odd
     u64* pos[2] = {(u64*)p, (u64*)p + K};
+    p += (size_t)2 * K * 8;
+    unsigned long long* flags = (unsigned long long*)p;     // [K][NT] look-back flags
+    cudaMemsetAsync(flags, 0, (size_t)K * NT * 8, st);
+    u32 seq = 0;
     cudaMemsetAsync(pos[0], 0, (size_t)K * sizeof(u64), st);
     A.a_out = a_out;
     A.e_out = e_out;
@@ -853,9 +924,8 @@ void keygen_streams_parallel(const Dev& d, int K, const void* streams, u64* cons
         for (int m = 0; m < d.L + 2; m++) {
             A.pos_in = pos[cur];
             A.pos_out = pos[cur ^ 1];
-            pk_gen_kernel<<<grid, RNG_T, 0, st>>>(A, 0, m);
-            pk_uniform_write<<<grid, RNG_T, 0, st>>>(A, digit, m);
-            note_launch(2);
+            pk_uniform_fused<<<grid, RNG_T, 0, st>>>(A, digit, m, flags, ++seq);
+            note_launch();
             cur ^= 1;
         }
         A.pos_in = pos[cur];
@@ -931,7 +1001,8 @@ struct JobKeyFused {
     u64* const* keys;
     const long long* e;          // [K][L+1][n]
     const u32* gal;
-    const u64* sk;               // [L+2][n]
+    const u64* sk;               // [L+2][n] then Shoup companions [L+2][n]
+    const u64* skp;              // [K][L+1][n] sk(X^g) per key (NTT-domain automorphism)
     const ulonglong2* f;         // [(L+1)^2]
     int per, L;
     Dev d;
@@ -940,18 +1011,22 @@ struct JobKeyFused {
         u64* a;
         const long long* e;
         const u64* skm;
+        const u64* skpm;
         ulonglong2 f;
-        u32 g;
         int m;
     };
     HS_DEV Ctx make(int jb) const {
-        const int kk = jb / per, limb = jb % per;
-        const int i = limb / (L + 2), m = limb % (L + 2);
+        // job order (key, modulus, digit): sk_m, its companion and sk(X^g)_m
+        // stay in L2 across the L+1 digits, e_i across the moduli of a key
+        const int kk = jb / per, r = jb % per;
+        const int m = r / (L + 1), i = r % (L + 1);
+        const int limb = i * (L + 2) + m;
         u64* key = keys[kk];
         const size_t half = (size_t)per * d.n;
         return Ctx{key + (size_t)limb * d.n, key + half + (size_t)limb * d.n,
                    e + ((size_t)kk * (L + 1) + i) * d.n, sk + (size_t)m * d.n,
-                   m <= L ? f[i * (L + 1) + m] : make_ulonglong2(0, 0), gal[kk], m};
+                   skp + ((size_t)kk * (L + 1) + (m <= L ? m : 0)) * d.n,
+                   m <= L ? f[i * (L + 1) + m] : make_ulonglong2(0, 0), m};
     }
     HS_DEV int prime(const Ctx& c) const { return c.m; }
     HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst& P) const {
@@ -963,12 +1038,7 @@ struct JobKeyFused {
     HS_DEV u64* scratch(const Ctx& c) const { return c.b; }
     HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst& P) const {
         u64 acc = csub(csub(v, P.two_q), P.q);
-        if (c.m <= L) {
-            const u32 br = __brev(j) >> (32 - d.log_n);
-            const u32 ex = (u32)((((u64)(2 * br + 1)) * c.g) & ((2ull << d.log_n) - 1));
-            const u32 pj = __brev((ex - 1) >> 1) >> (32 - d.log_n);
-            acc = add_mod(acc, shoup(c.skm[pj], c.f.x, c.f.y, P.q), P.q);
-        }
+        if (c.m <= L) acc = add_mod(acc, shoup(c.skpm[j], c.f.x, c.f.y, P.q), P.q);
         // a * sk with sk's Shoup companion (stored after the L+2 sk limbs)
         const u64 ask = csub(shoup_lazy(c.a[j], c.skm[j], c.skm[(size_t)(L + 2) * d.n + j], P.q), P.q);
         c.b[j] = sub_mod(acc, ask, P.q);
@@ -989,10 +1059,26 @@ void shoup_companions(const Dev& d, const u64* v, u64* sh, int nl, cudaStream_t 
     note_launch();
 }
 
+// skp[k][m][j] = sk[m][perm_g(j)]: the automorphism of the secret for key k,
+// gathered once per (key, modulus) instead of once per key limb.
+__global__ void sk_perm_kernel(Dev d, const u32* gal, const u64* sk, u64* skp) {
+    const u32 j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= d.n) return;
+    const int m = blockIdx.y, k = blockIdx.z;
+    const u32 br = __brev(j) >> (32 - d.log_n);
+    const u32 ex = (u32)((((u64)(2 * br + 1)) * gal[k]) & ((2ull << d.log_n) - 1));
+    const u32 pj = __brev((ex - 1) >> 1) >> (32 - d.log_n);
+    skp[((size_t)k * (d.L + 1) + m) * d.n + j] = sk[(size_t)m * d.n + pj];
+}
+
+size_t keygen_assemble_scratch_bytes(int K, const Dev& d) { return (size_t)K * (d.L + 1) * d.n * sizeof(u64); }
+
 void keygen_assemble(const Dev& d, int K, u64* const* keys, const long long* e, const u32* gal,
-                     const u64* sk, const ulonglong2* f, cudaStream_t st) {
+                     const u64* sk, const ulonglong2* f, u64* skp, cudaStream_t st) {
     const int per = (d.L + 1) * (d.L + 2);
-    launch_ntt<true>(d, JobKeyFused{keys, e, gal, sk, f, per, d.L, d}, K * per, st);
+    sk_perm_kernel<<<dim3((d.n + 255) / 256, d.L + 1, K), 256, 0, st>>>(d, gal, sk, skp);
+    note_launch();
+    launch_ntt<true>(d, JobKeyFused{keys, e, gal, sk, skp, f, per, d.L, d}, K * per, st);
 }
 
 size_t rng_jump_bytes() { return sizeof(RngJump); }
@@ -1100,7 +1186,8 @@ hs_status generate_galois_keys(hs_ctx* c, const std::vector<u32>& steps,
     const int L = c->L;
     const u32 n = c->n;
     const size_t half = (size_t)(L + 1) * (L + 2) * n;
-    const int KB = (int)std::max<size_t>(1, c->keygen_batch);
+    static const long kb_env = getenv("HS_KEYGEN_BATCH") ? atol(getenv("HS_KEYGEN_BATCH")) : 0;
+    const int KB = (int)std::max<size_t>(1, kb_env > 0 ? (size_t)kb_env : c->keygen_batch);
     long long* e = nullptr;
     u64** d_keys = nullptr;
     u64** d_aout = nullptr;
@@ -1111,6 +1198,8 @@ hs_status generate_galois_keys(hs_ctx* c, const std::vector<u32>& steps,
     HS_CUDA(cudaMallocAsync((void**)&d_aout, KB * sizeof(u64*), st));
     HS_CUDA(cudaMallocAsync((void**)&d_gal, KB * sizeof(u32), st));
     HS_CUDA(cudaMallocAsync((void**)&d_streams, KB * sizeof(hs_ctx::Stream), st));
+    u64* skp = nullptr;
+    HS_CUDA(cudaMallocAsync((void**)&skp, keygen_assemble_scratch_bytes(KB, c->dev), st));
     static const bool serial = getenv("HS_KEYGEN_SERIAL") != nullptr;
     void* par_scratch = nullptr;
     if (!serial) {
@@ -1139,7 +1228,7 @@ hs_status generate_galois_keys(hs_ctx* c, const std::vector<u32>& steps,
                                     par_scratch, c->d_kg_err, st);
         else
             keygen_streams(c->dev, K, d_streams, d_aout, e, c->d_jump, c->d_zig, c->d_thr, st);
-        keygen_assemble(c->dev, K, d_keys, e, d_gal, c->d_sk, c->d_kskf, st);
+        keygen_assemble(c->dev, K, d_keys, e, d_gal, c->d_sk, c->d_kskf, skp, st);
         // pageable host staging is copied at call time; device arrays are stream-ordered
         c->keys_generated += K;
     }
@@ -1149,6 +1238,7 @@ hs_status generate_galois_keys(hs_ctx* c, const std::vector<u32>& steps,
     cudaFreeAsync(d_aout, st);
     cudaFreeAsync(d_gal, st);
     cudaFreeAsync(d_streams, st);
+    cudaFreeAsync(skp, st);
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) {
         set_error(std::string("keygen launch failed: ") + cudaGetErrorString(err));

@@ -89,7 +89,8 @@ void keygen_streams_parallel(const Dev& d, int K, const void* streams, u64* cons
                              void* scratch, int* err, cudaStream_t st);
 void shoup_companions(const Dev& d, const u64* v, u64* sh, int nl, cudaStream_t st);
 void keygen_assemble(const Dev& d, int K, u64* const* keys, const long long* e, const u32* gal,
-                     const u64* sk, const ulonglong2* f, cudaStream_t st);
+                     const u64* sk, const ulonglong2* f, u64* skp, cudaStream_t st);
+size_t keygen_assemble_scratch_bytes(int K, const Dev& d);
 
 // data[i] mod q for limbs after an integer-sum collective
 void reduce_mod(const Dev& d, u64* data, int npoly, int nl, cudaStream_t st);
