@@ -239,34 +239,59 @@ struct JobModUp {                           // forward NTT, job = (b*(l+1)+i)*(l
 
 // Key inner product: ACC[b][c][m] = sum_i E[b][i][m][perm(k)] * K_b[c][i][m].
 // Keys are stored in standard form; redc128_std turns the 128-bit sum into
-// the plain residue.  grid = (n/256, l+2, B).
-__global__ void __launch_bounds__(256)
+// the plain residue.  Streaming kernel (HBM/L2 bound): each thread owns two
+// adjacent coefficients so key rows move as 16-byte loads and more loads are
+// in flight per thread.  grid = (ceil(n/512), l+2, B).
+constexpr int KSI_T = 256;
+
+__global__ void __launch_bounds__(KSI_T, 4)
 ks_inner_kernel(Dev d, int l, const u64* __restrict__ E, size_t e_item_stride,
                 const u64* const* __restrict__ keys, const u32* __restrict__ gal,
                 u64* __restrict__ ACC) {
     const u32 n = d.n;
-    const u32 k = blockIdx.x * blockDim.x + threadIdx.x;
+    const u32 k = 2 * (blockIdx.x * KSI_T + threadIdx.x);
     const int m = blockIdx.y;
     const int b = blockIdx.z;
     if (k >= n) return;
     const int pm = m <= l ? m : d.L + 1;
-    const PrimeConst P = d.pc[pm];
     const u32 g = gal ? gal[b] : 0u;
-    const u32 src = g ? galois_perm(k, g, d.log_n) : k;
-    const u64* Eb = E + (size_t)b * e_item_stride;
+    const u32 src0 = g ? galois_perm(k, g, d.log_n) : k;
+    const u32 src1 = g ? galois_perm(k + 1, g, d.log_n) : k + 1;
+    const u64* Eb = E + (size_t)b * e_item_stride + (size_t)m * n;
+    const size_t estride = (size_t)(l + 2) * n;                    // one digit of E
     const u64* key = keys[b];
-    const size_t kstride = (size_t)(d.L + 2) * n;                  // one digit
-    const u64* kb = key + (size_t)pm * n + k;
-    const u64* ka = key + (size_t)(d.L + 1) * kstride + (size_t)pm * n + k;
-    u64 lb = 0, hb = 0, la = 0, ha = 0;
+    const size_t kstride = (size_t)(d.L + 2) * n;                  // one digit of a key
+    const ulonglong2* kb = (const ulonglong2*)(key + (size_t)pm * n + k);
+    const ulonglong2* ka = (const ulonglong2*)(key + (size_t)(d.L + 1) * kstride + (size_t)pm * n + k);
+    const size_t kst2 = kstride / 2;
+    u64 lb0 = 0, hb0 = 0, la0 = 0, ha0 = 0, lb1 = 0, hb1 = 0, la1 = 0, ha1 = 0;
+#pragma unroll 2
     for (int i = 0; i <= l; i++) {
-        const u64 e = Eb[((size_t)i * (l + 2) + m) * n + src];
-        mac128(lb, hb, e, kb[(size_t)i * kstride]);
-        mac128(la, ha, e, ka[(size_t)i * kstride]);
+        const u64* Ei = Eb + (size_t)i * estride;
+        u64 e0, e1;
+        if (g) {
+            e0 = Ei[src0];
+            e1 = Ei[src1];
+        } else {
+            const ulonglong2 ee = *(const ulonglong2*)(Ei + k);
+            e0 = ee.x;
+            e1 = ee.y;
+        }
+        const ulonglong2 vb = kb[(size_t)i * kst2], va = ka[(size_t)i * kst2];
+        mac128(lb0, hb0, e0, vb.x);
+        mac128(lb1, hb1, e1, vb.y);
+        mac128(la0, ha0, e0, va.x);
+        mac128(la1, ha1, e1, va.y);
     }
+    const PrimeConst P = d.pc[pm];
     u64* out = ACC + (size_t)b * 2 * (l + 2) * n;
-    out[(size_t)m * n + k] = redc128_std(lb, hb, P);
-    out[((size_t)(l + 2) + m) * n + k] = redc128_std(la, ha, P);
+    *(ulonglong2*)(out + (size_t)m * n + k) = make_ulonglong2(redc128_std(lb0, hb0, P), redc128_std(lb1, hb1, P));
+    *(ulonglong2*)(out + ((size_t)(l + 2) + m) * n + k) =
+        make_ulonglong2(redc128_std(la0, ha0, P), redc128_std(la1, ha1, P));
+}
+
+static dim3 ks_inner_grid(const Dev& d, int l, int B) {
+    return dim3((d.n + 2 * KSI_T - 1) / (2 * KSI_T), l + 2, B);
 }
 
 // ModDown addends (what is added to the key-switch output), bound per CTA.
@@ -460,6 +485,18 @@ static void launch_modup_inner(const Dev& d, int B, int l, u64* D, u64* E, const
 // ModUp + inner product for B items (E must hold x_i df_i in slot (i, i)).
 static void modup_and_inner(const Dev& d, int B, int l, u64* D, u64* E, const u64* const* keys,
                             u64* ACC, cudaStream_t st) {
+    // Default: ModUp as a batched two-pass NTT writing E, then the streaming
+    // inner-product kernel (both run at high occupancy).  HS_MODUP_FUSED=1
+    // selects the fused pass-B + inner-product kernel (no E round trip, but
+    // 128-bit accumulators cap it at 25% occupancy).
+    static const bool fused = getenv("HS_MODUP_FUSED") != nullptr;
+    if (!fused) {
+        launch_ntt<true>(d, JobModUp{D, E, l, d.L, d.n, d.pc}, B * (l + 1) * (l + 1), st);
+        ks_inner_kernel<<<ks_inner_grid(d, l, B), KSI_T, 0, st>>>(d, l, E, (size_t)(l + 1) * (l + 2) * d.n,
+                                                                 keys, nullptr, ACC);
+        note_launch();
+        return;
+    }
     switch (d.log_n) {
         case 12: launch_modup_inner<6, 6>(d, B, l, D, E, keys, ACC, st); return;
         case 13: launch_modup_inner<6, 7>(d, B, l, D, E, keys, ACC, st); return;
@@ -471,8 +508,8 @@ static void modup_and_inner(const Dev& d, int B, int l, u64* D, u64* E, const u6
     }
     // small rings: whole-limb single-pass NTT, then the plain inner product
     launch_ntt<true>(d, JobModUp{D, E, l, d.L, d.n, d.pc}, B * (l + 1) * (l + 1), st);
-    dim3 g((d.n + 255) / 256, l + 2, B);
-    ks_inner_kernel<<<g, 256, 0, st>>>(d, l, E, (size_t)(l + 1) * (l + 2) * d.n, keys, nullptr, ACC);
+    ks_inner_kernel<<<ks_inner_grid(d, l, B), KSI_T, 0, st>>>(d, l, E, (size_t)(l + 1) * (l + 2) * d.n, keys,
+                                                             nullptr, ACC);
     note_launch();
 }
 
@@ -516,8 +553,7 @@ void rotate_hoisted(const Dev& d, int R, int l, const u64* src, const u32* gal,
     ItemPtr s = strided(src, 0);
     launch_ntt<false>(d, JobDecompose<SrcPlain>{SrcPlain{s, 1}, E, D, d.df, l, n, d}, l + 1, st);
     launch_ntt<true>(d, JobModUp{D, E, l, d.L, n, d.pc}, (l + 1) * (l + 1), st);
-    dim3 g((n + 255) / 256, l + 2, R);
-    ks_inner_kernel<<<g, 256, 0, st>>>(d, l, E, 0, keys, gal, ACC);
+    ks_inner_kernel<<<ks_inner_grid(d, l, R), KSI_T, 0, st>>>(d, l, E, 0, keys, gal, ACC);
     note_launch();
     mod_down(d, R, l, ACC, T, AddPermC0{s, gal}, out, st);
 }
