@@ -376,8 +376,9 @@ struct JobModDown {                          // forward NTT, job = (b*2+c)*(l+1)
     }
     HS_DEV u64* scratch(const Ctx& c) const { return c.out; }
     HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst& P) const {
-        u64 r = shoup(sub_mod(c.acc[j], canon4(v, P), P.q), c.w.x, c.w.y, P.q);
-        c.out[j] = add_mod(r, add.v(c.add, j, d, P), P.q);
+        // (acc - v) p^-1 + addend, one canonicalisation: acc < q, v < 4q
+        const u64 r = shoup_lazy(c.acc[j] + (P.two_q << 1) - v, c.w.x, c.w.y, P.q);   // [0, 2q)
+        c.out[j] = csub(csub(r + add.v(c.add, j, d, P), P.two_q), P.q);
     }
 };
 
@@ -591,9 +592,9 @@ struct JobRescale {                          // forward NTT, job = (b*npoly+c)*l
     }
     HS_DEV u64* scratch(const Ctx& c) const { return c.out; }
     HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst& P) const {
-        u64 r = shoup(sub_mod(c.x[j], canon4(v, P), P.q), c.w.x, c.w.y, P.q);
-        if (c.mask) r = mont_mul(r, c.mask[j], P.q, P.qinv_neg);
-        c.out[j] = r;
+        u64 r = shoup_lazy(c.x[j] + (P.two_q << 1) - v, c.w.x, c.w.y, P.q);            // [0, 2q)
+        if (c.mask) r = mont_mul_lazy(r, c.mask[j], P.q, P.qinv_neg);                 // [0, 2q)
+        c.out[j] = csub(r, P.q);
     }
 };
 
