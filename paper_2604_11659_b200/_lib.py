@@ -15,7 +15,7 @@ import subprocess
 from .errors import CapacityError, EvalError, KeyMissingError, ParameterError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libhespmm_b200.so")
+LIB_PATH = os.environ.get("HS_LIB_PATH") or os.path.join(_HERE, "lib", "libhespmm_b200.so")  # override: A/B tools
 CSRC = os.path.join(_HERE, "csrc")
 
 c_u64p = ctypes.POINTER(ctypes.c_uint64)

@@ -428,8 +428,11 @@ struct PassEngine {
     }
 };
 
+#ifndef NTT_MINB
+#define NTT_MINB 6
+#endif
 template <bool FWD, bool FIRST, bool LAST, int LOGG, int H, int C, int EPT, class Job>
-__global__ void __launch_bounds__(((H << LOGG) * C) / EPT)
+__global__ void __launch_bounds__(((H << LOGG) * C) / EPT, NTT_MINB)
 ntt_pass_kernel(Dev d, Job job, int s0, int jbase) {
     using PE = PassEngine<FWD, FIRST, LAST, LOGG, H, C, EPT, Job>;
     __shared__ u64 sm[2 * PE::SMW];
@@ -448,8 +451,11 @@ ntt_pass_kernel(Dev d, Job job, int s0, int jbase) {
     E.t = threadIdx.x;
     E.nq = 0ull - E.P.q;
     E.four_q = E.P.two_q << 1;
-    if (FWD && fwd_lazy_ok(E.P)) PE::template run<true>(sm, E, job);
-    else PE::template run<false>(sm, E, job);
+    // One code path for every prime: the lazy forward variant (run<true>,
+    // no upper-input reduction for sub-2^56 primes) saves ~5 instructions per
+    // butterfly but doubles the kernel's code, and instruction-cache misses
+    // cost more than that (A/B on B200: 194.9 vs 206.7 ms per cfg2 matmul).
+    PE::template run<false>(sm, E, job);
 }
 
 // Single-pass variant for small limbs (whole limb in one CTA, 8 per thread).
