@@ -186,7 +186,17 @@ def cpu_oracle_sample(wl, sample_pairs: int, nthreads: int):
 
 # ------------------------------------------------------------- roofline
 
-def roofline_probe(pkg, ctx, params, peaks):
+def roofline_traffic(workload: str):
+    """DRAM bytes per probe launch from the committed ncu capture of the same
+    probe (tools/roofline_probe.py -> profiles/r01_roofline_traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_roofline_traffic.json")) as fh:
+            return json.load(fh).get(workload)
+    except (OSError, ValueError):
+        return None
+
+
+def roofline_probe(pkg, ctx, params, peaks, reps=10, workload=None):
     """Time the dominant kernel alone with CUDA events on its launch stream.
 
     Dominant kernel: the NTT pass kernel (ntt_pass_kernel), which carries
@@ -204,9 +214,8 @@ def roofline_probe(pkg, ctx, params, peaks):
     limbs = items * (L + 1) * (L + 2)
     buf = D.zeros((limbs, n))
     st = torch.cuda.current_stream()
-    for _ in range(3):
+    for _ in range(3 if reps > 1 else 0):
         check(lib().hs_ntt(ctx.handle, D.ptr(buf), items * (L + 1), L + 2, 0, 0, D.stream()))
-    reps = 10
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     e0.record(st)
@@ -219,9 +228,12 @@ def roofline_probe(pkg, ctx, params, peaks):
     achieved = algo / (ms * 1e-3) / 1e9
     peak = peaks.get("hbm_gbs", 6650.0)
     butterflies = limbs * (n // 2) * (n.bit_length() - 1) / 2      # per pass
+    tr = roofline_traffic(workload) if workload else None
     return {"kernel": "ntt_pass_kernel (batched 2-pass NTT, one pass)", "bound": "hbm",
             "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": None,
+            "frac": round(achieved / peak, 4),
+            "traffic": tr["dram_bytes_per_launch"] if tr else None,
+            "traffic_source": tr["source"] if tr else None,
             "launch_ms": round(ms, 4), "algorithmic_bytes_per_launch": algo,
             "butterflies_per_launch": int(butterflies),
             "peak_source": "MEASURED_PEAKS.json" if "hbm_gbs" in peaks else "fallback"}
@@ -352,7 +364,7 @@ def run_b200_arm(args, wl):
     same = bool(np.array_equal(res.ctxt.host(), out))
 
     peaks = load_peaks()
-    roof = roofline_probe(pkg, ctx, params, peaks) if rank == 0 else None
+    roof = roofline_probe(pkg, ctx, params, peaks, workload=args.workload) if rank == 0 else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -395,7 +407,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
-    ap.add_argument("--cpu-sample-pairs", type=int, default=256)
+    ap.add_argument("--cpu-sample-pairs", type=int, default=1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]

@@ -257,27 +257,27 @@ ks_inner_kernel(Dev d, int l, const u64* __restrict__ E, size_t e_item_stride,
     const u32 g = gal ? gal[b] : 0u;
     const u32 src0 = g ? galois_perm(k, g, d.log_n) : k;
     const u32 src1 = g ? galois_perm(k + 1, g, d.log_n) : k + 1;
-    const u64* Eb = E + (size_t)b * e_item_stride + (size_t)m * n;
+    const u64* __restrict__ Ei = E + (size_t)b * e_item_stride + (size_t)m * n;
     const size_t estride = (size_t)(l + 2) * n;                    // one digit of E
     const u64* key = keys[b];
     const size_t kstride = (size_t)(d.L + 2) * n;                  // one digit of a key
-    const ulonglong2* kb = (const ulonglong2*)(key + (size_t)pm * n + k);
-    const ulonglong2* ka = (const ulonglong2*)(key + (size_t)(d.L + 1) * kstride + (size_t)pm * n + k);
+    const ulonglong2* __restrict__ kb = (const ulonglong2*)(key + (size_t)pm * n + k);
+    const ulonglong2* __restrict__ ka =
+        (const ulonglong2*)(key + (size_t)(d.L + 1) * kstride + (size_t)pm * n + k);
     const size_t kst2 = kstride / 2;
     u64 lb0 = 0, hb0 = 0, la0 = 0, ha0 = 0, lb1 = 0, hb1 = 0, la1 = 0, ha1 = 0;
 #pragma unroll 2
-    for (int i = 0; i <= l; i++) {
-        const u64* Ei = Eb + (size_t)i * estride;
+    for (int i = 0; i <= l; i++, Ei += estride, kb += kst2, ka += kst2) {
         u64 e0, e1;
         if (g) {
-            e0 = Ei[src0];
-            e1 = Ei[src1];
+            e0 = __ldg(Ei + src0);
+            e1 = __ldg(Ei + src1);
         } else {
-            const ulonglong2 ee = *(const ulonglong2*)(Ei + k);
+            const ulonglong2 ee = __ldg((const ulonglong2*)(Ei + k));
             e0 = ee.x;
             e1 = ee.y;
         }
-        const ulonglong2 vb = kb[(size_t)i * kst2], va = ka[(size_t)i * kst2];
+        const ulonglong2 vb = __ldg(kb), va = __ldg(ka);
         mac128(lb0, hb0, e0, vb.x);
         mac128(lb1, hb1, e1, vb.y);
         mac128(la0, ha0, e0, va.x);
