@@ -250,6 +250,11 @@ void hs_ctx_destroy(hs_ctx* c) {
     for (void* p : {(void*)c->d_jump, (void*)c->d_zig, (void*)c->d_thr, (void*)c->d_sk, (void*)c->d_kskf})
         if (p) cudaFree(p);
     if (c->d_blob) cudaFree(c->d_blob);
+    if (c->d_kg_err) cudaFree(c->d_kg_err);
+    for (auto s : c->kg_stream)
+        if (s) cudaStreamDestroy(s);
+    for (auto e : c->kg_event)
+        if (e) cudaEventDestroy(e);
     delete c;
 }
 

@@ -56,9 +56,12 @@ struct hs_ctx {
     ulonglong2* d_kskf = nullptr;            // p (Q_L/q_i) mod q_m, Shoup pairs [(L+1)^2]
     struct Stream { u64 s_hi, s_lo, i_hi, i_lo; };
     std::unordered_map<u32, Stream> lazy;    // registered steps generated on demand
-    size_t keygen_batch = 16;                // keys generated per launch
+    size_t keygen_batch = 64;                // keys generated per launch (per-launch latency amortised)
     int64_t keys_generated = 0;
     int* d_kg_err = nullptr;                 // set if a keygen stream window overflowed
+    static constexpr int KG_LANES = 4;       // concurrent key-generation chains
+    cudaStream_t kg_stream[KG_LANES] = {};   // (latency-bound launches overlap across chains)
+    cudaEvent_t kg_event[KG_LANES + 1] = {};
     hs::KeyBuf relin;
     size_t batch_bytes = (size_t)6 << 30;   // runner work-buffer budget
     std::unordered_map<u32, hs::KeyBuf> galois;   // normalised step -> key

@@ -1207,7 +1207,8 @@ hs_status generate_galois_keys(hs_ctx* c, const std::vector<u32>& steps,
             HS_CUDA(cudaMalloc((void**)&c->d_kg_err, sizeof(int)));
             HS_CUDA(cudaMemset(c->d_kg_err, 0, sizeof(int)));
         }
-        HS_CUDA(cudaMallocAsync(&par_scratch, keygen_par_scratch_bytes(KB, c->n), st));
+        // room for KG_LANES sub-chunk slices, each 256-byte aligned
+        HS_CUDA(cudaMallocAsync(&par_scratch, keygen_par_scratch_bytes(KB, c->n) + hs_ctx::KG_LANES * 512, st));
     }
     for (size_t k0 = 0; k0 < steps.size(); k0 += KB) {
         const int K = (int)std::min<size_t>(KB, steps.size() - k0);
@@ -1223,12 +1224,37 @@ hs_status generate_galois_keys(hs_ctx* c, const std::vector<u32>& steps,
         HS_CUDA(cudaMemcpyAsync(d_gal, gal.data(), K * sizeof(u32), cudaMemcpyHostToDevice, st));
         HS_CUDA(cudaMemcpyAsync(d_streams, streams.data() + k0, K * sizeof(hs_ctx::Stream),
                                 cudaMemcpyHostToDevice, st));
-        if (par_scratch)
-            keygen_streams_parallel(c->dev, K, d_streams, d_aout, e, c->d_jump, c->d_zig, c->d_thr,
-                                    par_scratch, c->d_kg_err, st);
-        else
+        if (par_scratch) {
+            // split the chunk over concurrent chains: each chain's launches are
+            // latency-bound (small grids, serial segment chain), so chains overlap
+            static const int lanes_env = getenv("HS_KEYGEN_LANES") ? atoi(getenv("HS_KEYGEN_LANES")) : 0;
+            const int lanes = lanes_env > 0 ? std::min(lanes_env, (int)hs_ctx::KG_LANES) : 1;   // A/B: 1 lane fastest at K=12..23
+            const int S = std::min(K, lanes);
+            if (!c->kg_stream[0]) {
+                for (int j = 0; j < hs_ctx::KG_LANES; j++)
+                    HS_CUDA(cudaStreamCreateWithFlags(&c->kg_stream[j], cudaStreamNonBlocking));
+                for (int j = 0; j <= hs_ctx::KG_LANES; j++)
+                    HS_CUDA(cudaEventCreateWithFlags(&c->kg_event[j], cudaEventDisableTiming));
+            }
+            HS_CUDA(cudaEventRecord(c->kg_event[hs_ctx::KG_LANES], st));
+            size_t soff = 0;
+            for (int j = 0; j < S; j++) {
+                const int ka = K * j / S, kc = K * (j + 1) / S - ka;
+                cudaStream_t sj = c->kg_stream[j];
+                HS_CUDA(cudaStreamWaitEvent(sj, c->kg_event[hs_ctx::KG_LANES], 0));
+                keygen_streams_parallel(c->dev, kc, d_streams + ka, d_aout + ka, e + (size_t)ka * (L + 1) * n,
+                                        c->d_jump, c->d_zig, c->d_thr, (char*)par_scratch + soff,
+                                        c->d_kg_err, sj);
+                soff += (keygen_par_scratch_bytes(kc, c->n) + 255) & ~(size_t)255;
+                keygen_assemble(c->dev, kc, d_keys + ka, e + (size_t)ka * (L + 1) * n, d_gal + ka, c->d_sk,
+                                c->d_kskf, skp + (size_t)ka * (L + 1) * n, sj);
+                HS_CUDA(cudaEventRecord(c->kg_event[j], sj));
+            }
+            for (int j = 0; j < S; j++) HS_CUDA(cudaStreamWaitEvent(st, c->kg_event[j], 0));
+        } else {
             keygen_streams(c->dev, K, d_streams, d_aout, e, c->d_jump, c->d_zig, c->d_thr, st);
-        keygen_assemble(c->dev, K, d_keys, e, d_gal, c->d_sk, c->d_kskf, skp, st);
+            keygen_assemble(c->dev, K, d_keys, e, d_gal, c->d_sk, c->d_kskf, skp, st);
+        }
         // pageable host staging is copied at call time; device arrays are stream-ordered
         c->keys_generated += K;
     }

@@ -57,7 +57,9 @@ HS_DEV u64 mulhi_apx(u64 x, u64 y) {
 // x*w - Q*q is formed as x*w + Q*(2^64 - q) (nq) so the chain is pure IMADs.
 HS_DEV u64 shoup_ex(u64 x, u64 w, u64 w_sh, u64 nq) { return x * w + mulhi_ex(x, w_sh) * nq; }
 
-// Approximate-quotient Shoup product in 11 integer instructions:
+// Approximate-quotient Shoup product in 11 IMADs (all on the FMA pipe; the
+// 64-bit accumulations use IMAD.WIDE with a unit multiplier so no register
+// pair has to be assembled with MOVs):
 //   Q = x1 s1 + hi(x1 s0) + hi(x0 s1)               (Q in [Q_exact - 2, Q_exact])
 //   r = lo64(x w + Q nq)                              (r in [0, 4q))
 HS_DEV u64 shoup_ax(u64 x, u64 w, u64 w_sh, u64 nq) {
@@ -72,11 +74,9 @@ HS_DEV u64 shoup_ax(u64 x, u64 w, u64 w_sh, u64 nq) {
         "mul.hi.u32 a, x1, s0;\n\t"
         "mul.hi.u32 b, x0, s1;\n\t"
         "mul.wide.u32 Q, x1, s1;\n\t"
+        "mad.wide.u32 Q, a, 1, Q;\n\t"
+        "mad.wide.u32 Q, b, 1, Q;\n\t"
         "mov.b64 {q0, q1}, Q;\n\t"
-        "add.cc.u32 q0, q0, a;\n\t"
-        "addc.u32 q1, q1, 0;\n\t"
-        "add.cc.u32 q0, q0, b;\n\t"
-        "addc.u32 q1, q1, 0;\n\t"
         "mul.wide.u32 T, x0, w0;\n\t"
         "mad.wide.u32 T, q0, n0, T;\n\t"
         "mov.b64 {t0, t1}, T;\n\t"
