@@ -53,6 +53,12 @@ WORKLOADS = {
     "cfg3s": dict(ring_degree=1 << 16, scale_bits=50, levels=24, seed=2024, dim=32, sparsity=0.9,
                   lazy_keys=True, batch_gb=16,
                   desc="N=2^16, L=24, 32x32 @90% (cfg3 parameters, smaller matrix)"),
+    # configs[3] scale: 256x256 needs 65,536 slots > 32,768 at N=2^16 -> 2x2 tiles of 128x128
+    # (tiling.py; beyond the reference's one-ciphertext capacity)
+    "cfg4s": dict(ring_degree=1 << 16, scale_bits=50, levels=24, seed=2024, dim=256, sparsity=0.99,
+                  lazy_keys=True, batch_gb=16, tiled=True,
+                  desc="configs[3] scale: N=2^16, L=24, 256x256 @99% as 2x2 tiles of 128x128 "
+                       "ciphertexts (multi-ciphertext tiling)"),
 }
 
 
@@ -128,21 +134,48 @@ def make_inputs(pkg, wl):
     seed = cell_seed(wl["dim"])
     a = formats.generate_random_sparse(wl["dim"], wl["sparsity"], (seed, 0))
     b = formats.generate_random_sparse(wl["dim"], wl["sparsity"], (seed, 1))
-    ea = encmat.encrypt_sparse(a, encmat.Layout.CSR, ctx, keys)
-    eb = encmat.encrypt_sparse(b, encmat.Layout.CSC, ctx, keys)
-    steps = encmat.required_rotation_steps(ea.meta, eb.meta)
+    if wl.get("tiled"):
+        from paper_2604_11659_b200 import tiling
+        ea = tiling.encrypt_tiled(a, encmat.Layout.CSR, ctx, keys)
+        eb = tiling.encrypt_tiled(b, encmat.Layout.CSC, ctx, keys)
+        steps = tiling.required_rotation_steps_tiled(ea, eb)
+        blk = [encmat.pair_array(ea.tiles[(I, K)].meta, eb.tiles[(K, J)].meta)
+               for I, K, J in tiling.block_products(ea, eb)]
+        pairs = np.concatenate([p for p in blk if len(p)]) if blk else np.zeros((0, 4), np.int64)
+        mc = engine.MaskCache(ctx, ea.b)
+    else:
+        ea = encmat.encrypt_sparse(a, encmat.Layout.CSR, ctx, keys)
+        eb = encmat.encrypt_sparse(b, encmat.Layout.CSC, ctx, keys)
+        steps = encmat.required_rotation_steps(ea.meta, eb.meta)
+        pairs = encmat.pair_array(ea.meta, eb.meta)
+        mc = engine.MaskCache(ctx, wl["dim"])
     keys = ctx.gen_galois_keys(steps, keys, device="lazy" if wl.get("lazy_keys") else False)
     if wl.get("batch_gb"):
         from paper_2604_11659_b200._lib import lib
         lib().hs_set_batch_bytes(ctx.handle, int(wl["batch_gb"]) << 30)
-    pairs = encmat.pair_array(ea.meta, eb.meta)
-    mc = engine.MaskCache(ctx, wl["dim"])
     mc.prewarm(np.unique(np.minimum(pairs[:, 2], pairs[:, 3])))
     import torch
     torch.cuda.synchronize()
     log(f"[bench] setup {time.time() - t0:.1f}s: {len(pairs)} pairs, {len(steps)} rotation steps, "
         f"{len(keys.galois)} Galois keys")
     return params, ctx, keys, a, b, ea, eb, pairs, mc
+
+
+def workload_ct_ops(ea, eb, dim: int) -> int:
+    """Logical OpCounter total of one step: the reference's count for the
+    schedule, summed over block products (+ the adds joining partial blocks)
+    for a tiled workload."""
+    from paper_2604_11659_b200 import encmat
+    if hasattr(ea, "tiles"):
+        from paper_2604_11659_b200 import tiling
+        total, outs = 0, {}
+        for I, K, J in tiling.block_products(ea, eb):
+            p = encmat.pair_array(ea.tiles[(I, K)].meta, eb.tiles[(K, J)].meta)
+            if len(p):
+                total += logical_ct_ops(p, ea.b)
+                outs[(I, J)] = outs.get((I, J), 0) + 1
+        return total + sum(v - 1 for v in outs.values())
+    return logical_ct_ops(encmat.pair_array(ea.meta, eb.meta), dim)
 
 
 def logical_ct_ops(pairs: np.ndarray, dim: int) -> int:
@@ -253,6 +286,10 @@ def run_reference_arm(args, wl):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    if wl.get("tiled"):
+        print(json.dumps({"impl": "reference", "unavailable": "the reference packs one matrix per "
+                          "ciphertext and raises CapacityError beyond its slots (no tiling)"}))
+        return
     nthreads = os.cpu_count() or 1
     for _ in range(args.warmup):
         pass                                    # the CPU oracle has no warm-up state
@@ -298,13 +335,37 @@ def run_b200_arm(args, wl):
 
     params, ctx, keys, a, b, ea, eb, pairs, mc = make_inputs(pkg, wl)
     dim = wl["dim"]
-    ct_ops = logical_ct_ops(pairs, dim)
+    ct_ops = workload_ct_ops(ea, eb, dim)
+    tiled = bool(wl.get("tiled"))
+    from paper_2604_11659_b200 import tiling
 
     def step(ea_, eb_):
         c = engine.OpCounter()
-        if world > 1:
-            return hdist.spmm_csr_csc_distributed(ea_, eb_, ctx, keys, c, mc), c
-        return engine.spmm_csr_csc(ea_, eb_, ctx, keys, c, mc), c
+        spmm = hdist.spmm_csr_csc_distributed if world > 1 else engine.spmm_csr_csc
+        if tiled:
+            return tiling.spmm_tiled(ea_, eb_, ctx, keys, c, mc, spmm=spmm), c
+        return spmm(ea_, eb_, ctx, keys, c, mc), c
+
+    def result_host(r):
+        if tiled:
+            return np.concatenate([r.tiles[k].ctxt.host().ravel() for k in sorted(r.tiles)])
+        return r.ctxt.host()
+
+    def operand_host(e):
+        """Pinned host copy of an operand (ciphertext limbs only; metadata is plaintext)."""
+        if tiled:
+            return {k: torch.from_numpy(t.ctxt.host()).pin_memory() for k, t in e.tiles.items()}
+        return torch.from_numpy(e.ctxt.host()).pin_memory()
+
+    def operand_from_host(e, h):
+        if tiled:
+            return tiling.TiledMatrix(e.n, e.T, e.b, e.layout, {
+                k: encmat.EncryptedSparseMatrix(Ciphertext(h[k], t.ctxt.scale, t.ctxt.level), t.meta)
+                for k, t in e.tiles.items()})
+        return encmat.EncryptedSparseMatrix(Ciphertext(h, e.ctxt.scale, e.ctxt.level), e.meta)
+
+    def host_bytes(h):
+        return sum(x.numel() * 8 for x in h.values()) if tiled else h.numel() * 8
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
     res, c = step(ea, eb)
@@ -338,8 +399,8 @@ def run_b200_arm(args, wl):
     value = ct_ops / (ms * 1e-3)
 
     # ---- end to end through the public API from pinned host buffers
-    host_a = torch.from_numpy(ea.ctxt.host()).pin_memory()
-    host_b = torch.from_numpy(eb.ctxt.host()).pin_memory()
+    host_a = operand_host(ea)
+    host_b = operand_host(eb)
     e2e_s = 0.0
     d2h = 0
     for _ in range(args.steps):
@@ -348,10 +409,10 @@ def run_b200_arm(args, wl):
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        ha = encmat.EncryptedSparseMatrix(Ciphertext(host_a, ea.ctxt.scale, ea.ctxt.level), ea.meta)
-        hb = encmat.EncryptedSparseMatrix(Ciphertext(host_b, eb.ctxt.scale, eb.ctxt.level), eb.meta)
+        ha = operand_from_host(ea, host_a)
+        hb = operand_from_host(eb, host_b)
         r, _ = step(ha, hb)
-        out = r.ctxt.host()
+        out = result_host(r)
         e2e_s += time.perf_counter() - t0
         d2h = out.nbytes
     if world > 1:
@@ -361,13 +422,13 @@ def run_b200_arm(args, wl):
     e2e_value = ct_ops / (e2e_s / args.steps)
 
     # ---- bit-exactness spot check of the timed result (cheap: vs the first run)
-    same = bool(np.array_equal(res.ctxt.host(), out))
+    same = bool(np.array_equal(result_host(res), out))
 
     peaks = load_peaks()
     roof = roofline_probe(pkg, ctx, params, peaks, workload=args.workload) if rank == 0 else None
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not tiled:
         nthreads = os.cpu_count() or 1
         dt, ops_s, used = cpu_oracle_sample(wl, args.cpu_sample_pairs, nthreads)
         cpu = {"value": ops_s / dt, "unit": "ct-ops/s", "cores": nthreads, "kind": "port",
@@ -387,7 +448,7 @@ def run_b200_arm(args, wl):
                        "galois_keys": len(keys.galois), "parallelism": f"pair-shard x{world}",
                        "l2": "flushed between steps (256 MiB write)"},
             "e2e": {"value": e2e_value, "unit": "ct-ops/s",
-                    "h2d_bytes_per_step": int(host_a.numel() * 8 + host_b.numel() * 8),
+                    "h2d_bytes_per_step": int(host_bytes(host_a) + host_bytes(host_b)),
                     "d2h_bytes_per_step": int(d2h), "ms_per_matmul": e2e_s / args.steps * 1e3},
             "gpu_launches": int(launches),
             "roofline": roof,
