@@ -29,6 +29,8 @@
 // used in place between passes.  Fusions (basis lift on load, key-switch /
 // rescale epilogues on store) are expressed as Job types in ops.cu.
 #pragma once
+#include <type_traits>
+
 #include "hs_internal.cuh"
 
 namespace hs {
@@ -199,7 +201,10 @@ __device__ __forceinline__ void ntt_rounds_fwd(u64* sm, const ulonglong2* tw, u3
 // when EPT = 8).  Each thread holds EPT elements; in round r it owns
 // EPT / 2^R "units" -- the 2^R elements that differ only in the round's bits
 // -- and performs all their butterflies in registers.
-constexpr int NTT_EPT16 = 16;
+#ifndef NTT_EPT_BIG
+#define NTT_EPT_BIG 16
+#endif
+constexpr int NTT_EPT16 = NTT_EPT_BIG;   // elements per thread of the two-pass kernels (A/B knob)
 
 template <int LOGG, int EPT>
 struct Plan {
@@ -429,10 +434,13 @@ struct PassEngine {
 };
 
 #ifndef NTT_MINB
-#define NTT_MINB 6
+#define NTT_MINB 6            // CTAs/SM for 16 elements per thread (128 threads)
+#endif
+#ifndef NTT_MINB8
+#define NTT_MINB8 4           // for 8 elements per thread (256 threads)
 #endif
 template <bool FWD, bool FIRST, bool LAST, int LOGG, int H, int C, int EPT, class Job>
-__global__ void __launch_bounds__(((H << LOGG) * C) / EPT, NTT_MINB)
+__global__ void __launch_bounds__(((H << LOGG) * C) / EPT, EPT >= 16 ? NTT_MINB : NTT_MINB8)
 ntt_pass_kernel(Dev d, Job job, int s0, int jbase) {
     using PE = PassEngine<FWD, FIRST, LAST, LOGG, H, C, EPT, Job>;
     __shared__ u64 sm[2 * PE::SMW];
@@ -468,6 +476,19 @@ void launch_ntt_single(const Dev& d, const Job& job, int jbase, int njobs, cudaS
     note_launch();
 }
 
+// Elements per thread of a job's column pass (A) and row pass (B): 16 unless
+// the job declares kEptA / kEptB = 8 (256 threads).  No job does: per-kernel
+// A/B at cfg2 favoured 8 for a few loader/epilogue-heavy passes (-3.7% of
+// kernel time) but the same choice cost 45% at N = 2^16, L = 24.
+template <class J, class = void>
+struct EptA { static constexpr int value = NTT_EPT16; };
+template <class J>
+struct EptA<J, std::void_t<decltype(J::kEptA)>> { static constexpr int value = J::kEptA; };
+template <class J, class = void>
+struct EptB { static constexpr int value = NTT_EPT16; };
+template <class J>
+struct EptB<J, std::void_t<decltype(J::kEptB)>> { static constexpr int value = J::kEptB; };
+
 // Two-pass variant: pass A covers stages [0, LA) over strided columns, pass B
 // covers [LA, log n) over contiguous rows.  Forward runs A then B; inverse
 // runs B then A.
@@ -475,16 +496,16 @@ template <bool FWD, int LA, int LB, class Job>
 void launch_ntt_two(const Dev& d, const Job& job, int jbase, int njobs, cudaStream_t st) {
     constexpr int CA = NTT_TILE >> LA;   // columns per tile in pass A
     constexpr int HB = NTT_TILE >> LB;   // rows per tile in pass B
-    constexpr int TH = NTT_TILE / NTT_EPT16;
+    constexpr int EA = EptA<Job>::value, EB = EptB<Job>::value;
     const u32 n = 1u << (LA + LB);
     dim3 grid(n / NTT_TILE, njobs);
     note_launch(2);
     if constexpr (FWD) {
-        ntt_pass_kernel<true, true, false, LA, 1, CA, NTT_EPT16, Job><<<grid, TH, 0, st>>>(d, job, 0, jbase);
-        ntt_pass_kernel<true, false, true, LB, HB, 1, NTT_EPT16, Job><<<grid, TH, 0, st>>>(d, job, LA, jbase);
+        ntt_pass_kernel<true, true, false, LA, 1, CA, EA, Job><<<grid, NTT_TILE / EA, 0, st>>>(d, job, 0, jbase);
+        ntt_pass_kernel<true, false, true, LB, HB, 1, EB, Job><<<grid, NTT_TILE / EB, 0, st>>>(d, job, LA, jbase);
     } else {
-        ntt_pass_kernel<false, true, false, LB, HB, 1, NTT_EPT16, Job><<<grid, TH, 0, st>>>(d, job, LA, jbase);
-        ntt_pass_kernel<false, false, true, LA, 1, CA, NTT_EPT16, Job><<<grid, TH, 0, st>>>(d, job, 0, jbase);
+        ntt_pass_kernel<false, true, false, LB, HB, 1, EB, Job><<<grid, NTT_TILE / EB, 0, st>>>(d, job, LA, jbase);
+        ntt_pass_kernel<false, false, true, LA, 1, CA, EA, Job><<<grid, NTT_TILE / EA, 0, st>>>(d, job, 0, jbase);
     }
 }
 
