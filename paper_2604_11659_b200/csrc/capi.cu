@@ -55,6 +55,7 @@ PrimeConst make_prime_const(u64 q, u32 n) {
     P.r_mod = (u64)(((u128)1 << 64) % q);
     P.r2_mod = (u64)((u128)P.r_mod * P.r_mod % q);
     P.m64 = (u64)(((u128)1 << 64) / q);
+    P.r_sh = (u64)(((u128)P.r_mod << 64) / q);
     if (n) {
         P.n_inv = invmod(n, q);
         P.n_inv_sh = (u64)(((u128)P.n_inv << 64) / q);

@@ -23,6 +23,7 @@ struct PrimeConst {
     u64 r2_mod;      // 2^128 mod q  (to enter Montgomery form)
     u64 n_inv, n_inv_sh;
     u64 m64;         // floor(2^64 / q): generic 64-bit Barrett (reduce64)
+    u64 r_sh;        // floor(r_mod 2^64 / q): Shoup companion of 2^64 mod q
     u32 k;           // bitlen(q)
     u32 pad;
 };

@@ -50,6 +50,14 @@ HS_DEV u64 redc128_std(u64 lo, u64 hi, const PrimeConst& P) {
     return mont_mul(redc128(lo, hi, P), P.r2_mod, P.q, P.qinv_neg);
 }
 
+// hi 2^64 + lo mod q for any hi, lo < 2^64: hi (2^64 mod q) by Shoup plus
+// lo mod q (Barrett), one exact canonical result.  Cheaper than REDC + the
+// Montgomery correction (redc128_std) for standard-form keys.
+HS_DEV u64 reduce128(u64 lo, u64 hi, const PrimeConst& P) {
+    const u64 t = shoup_lazy(hi, P.r_mod, P.r_sh, P.q) + reduce64(lo, P);     // < 3q
+    return csub(csub(t, P.two_q), P.q);
+}
+
 // Barrett reduction of a 128-bit value x < 2 q^2 (same estimate as mul_mod).
 HS_DEV u64 barrett128(u64 lo, u64 hi, const PrimeConst& P) {
     u64 q1 = (hi << (65 - P.k)) | (lo >> (P.k - 1));
@@ -285,9 +293,9 @@ ks_inner_kernel(Dev d, int l, const u64* __restrict__ E, size_t e_item_stride,
     }
     const PrimeConst P = d.pc[pm];
     u64* out = ACC + (size_t)b * 2 * (l + 2) * n;
-    *(ulonglong2*)(out + (size_t)m * n + k) = make_ulonglong2(redc128_std(lb0, hb0, P), redc128_std(lb1, hb1, P));
+    *(ulonglong2*)(out + (size_t)m * n + k) = make_ulonglong2(reduce128(lb0, hb0, P), reduce128(lb1, hb1, P));
     *(ulonglong2*)(out + ((size_t)(l + 2) + m) * n + k) =
-        make_ulonglong2(redc128_std(la0, ha0, P), redc128_std(la1, ha1, P));
+        make_ulonglong2(reduce128(la0, ha0, P), reduce128(la1, ha1, P));
 }
 
 static dim3 ks_inner_grid(const Dev& d, int l, int B) {
