@@ -252,6 +252,10 @@ void hs_ctx_destroy(hs_ctx* c) {
         if (p) cudaFree(p);
     if (c->d_blob) cudaFree(c->d_blob);
     if (c->d_kg_err) cudaFree(c->d_kg_err);
+    for (u64* b : c->kpool_buf) cudaFree(b);
+    for (auto e : c->kpool_gen_ev) cudaEventDestroy(e);
+    for (auto e : c->kpool_use_ev) cudaEventDestroy(e);
+    if (c->kpool_side) cudaStreamDestroy(c->kpool_side);
     for (auto s : c->kg_stream)
         if (s) cudaStreamDestroy(s);
     for (auto e : c->kg_event)

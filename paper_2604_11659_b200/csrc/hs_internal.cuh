@@ -59,6 +59,12 @@ struct hs_ctx {
     size_t keygen_batch = 64;                // keys generated per launch (per-launch latency amortised)
     int64_t keys_generated = 0;
     int* d_kg_err = nullptr;                 // set if a keygen stream window overflowed
+    // Buffers of the runner's generated-key pool, kept across calls (cudaMalloc
+    // of tens of GB per call dominated and varied the step time); contents
+    // are NOT reused across calls -- every call regenerates the keys it uses.
+    std::vector<u64*> kpool_buf;
+    std::vector<cudaEvent_t> kpool_gen_ev, kpool_use_ev;
+    cudaStream_t kpool_side = nullptr;
     static constexpr int KG_LANES = 4;       // concurrent key-generation chains
     cudaStream_t kg_stream[KG_LANES] = {};   // (latency-bound launches overlap across chains)
     cudaEvent_t kg_event[KG_LANES + 1] = {};

@@ -296,8 +296,11 @@ HS_DEV void unit_butterflies(u64* v, const ulonglong2* __restrict__ tw, u32 Y, u
 // [0, 4q) in both directions.  Internal invariants: forward LZ values grow
 // by < 4q per stage from < 4q; forward Harvey values stay in [0, 8q) (csub
 // by 4q, approximate Shoup in [0, 4q)); inverse values stay in [0, 4q).
-template <bool FWD, bool FIRST, bool LAST, int LOGG, int H, int C, int EPT, class Job>
+// LOGN (log2 ring degree) and S0 (first stage of the pass) are template
+// parameters so every index shift/mask below is a compile-time constant.
+template <bool FWD, bool FIRST, bool LAST, int LOGG, int H, int C, int EPT, int LOGN, int S0, class Job>
 struct PassEngine {
+    static constexpr int LO_BITS = LOGN - S0 - LOGG;   // bits below the pass's range
     using PL = Plan<LOGG, EPT>;
     static constexpr int G = 1 << LOGG;
     static constexpr int TILE = H * G * C;
@@ -314,10 +317,9 @@ struct PassEngine {
         PrimeConst P;
         const ulonglong2* __restrict__ tw;
         u32 t, hi0, lo0;
-        int log_n, s0, lo_bits;
         u64 nq, four_q;
         HS_DEV u32 gidx(u32 h, u32 g, u32 c) const {
-            return ((hi0 + h) << (log_n - s0)) | (g << lo_bits) | (lo0 + c);
+            return ((hi0 + h) << (LOGN - S0)) | (g << LO_BITS) | (lo0 + c);
         }
     };
 
@@ -363,7 +365,7 @@ struct PassEngine {
 #pragma unroll
         for (int k = 0; k < M::UPT; k++) {
             const auto u = M::unit(E.t + k * T);
-            const u32 Y = (((1u << E.s0) + E.hi0 + u.h) << M::AA) + u.gh;
+            const u32 Y = (((1u << S0) + E.hi0 + u.h) << M::AA) + u.gh;
             unit_butterflies<FWD, LZ, M::RR>(v + k * M::NU, E.tw, Y, E.nq, E.P.two_q, E.four_q);
         }
     }
@@ -390,7 +392,7 @@ struct PassEngine {
         using ML = RM<RLAST>;
         // ---- load
         if constexpr (MF::direct) {
-            const u32 gstride = 1u << (MF::LOWB + E.lo_bits);
+            constexpr u32 gstride = 1u << (MF::LOWB + LO_BITS);
 #pragma unroll
             for (int k = 0; k < MF::UPT; k++) {
                 const auto u = MF::unit(E.t + k * T);
@@ -412,7 +414,7 @@ struct PassEngine {
         rest<1, LZ>(sm, v, E);
         // ---- store
         if constexpr (ML::direct) {
-            const u32 gstride = 1u << (ML::LOWB + E.lo_bits);
+            constexpr u32 gstride = 1u << (ML::LOWB + LO_BITS);
 #pragma unroll
             for (int k = 0; k < ML::UPT; k++) {
                 const auto u = ML::unit(E.t + k * T);
@@ -439,21 +441,18 @@ struct PassEngine {
 #ifndef NTT_MINB8
 #define NTT_MINB8 4           // for 8 elements per thread (256 threads)
 #endif
-template <bool FWD, bool FIRST, bool LAST, int LOGG, int H, int C, int EPT, class Job>
+template <bool FWD, bool FIRST, bool LAST, int LOGG, int H, int C, int EPT, int LOGN, int S0, class Job>
 __global__ void __launch_bounds__(((H << LOGG) * C) / EPT, EPT >= 16 ? NTT_MINB : NTT_MINB8)
-ntt_pass_kernel(Dev d, Job job, int s0, int jbase) {
-    using PE = PassEngine<FWD, FIRST, LAST, LOGG, H, C, EPT, Job>;
+ntt_pass_kernel(Dev d, Job job, int jbase) {
+    using PE = PassEngine<FWD, FIRST, LAST, LOGG, H, C, EPT, LOGN, S0, Job>;
     __shared__ u64 sm[2 * PE::SMW];
     typename PE::Env E;
     const int jb = jbase + (int)blockIdx.y;
     E.jc = job.make(jb);
     const int p = job.prime(E.jc);
     E.P = d.pc[p];
-    E.tw = (FWD ? d.tw : d.itw) + (size_t)p * d.n;
-    E.log_n = d.log_n;
-    E.s0 = s0;
-    E.lo_bits = d.log_n - s0 - LOGG;
-    const u32 ncolblk = (1u << E.lo_bits) / C;
+    E.tw = (FWD ? d.tw : d.itw) + ((size_t)p << LOGN);
+    constexpr u32 ncolblk = (1u << PE::LO_BITS) / C;
     E.hi0 = (blockIdx.x / ncolblk) * H;
     E.lo0 = (blockIdx.x % ncolblk) * C;
     E.t = threadIdx.x;
@@ -472,7 +471,7 @@ void launch_ntt_single(const Dev& d, const Job& job, int jbase, int njobs, cudaS
     dim3 grid(1, njobs);
     constexpr int EPT = LOGN >= 3 ? 8 : (1 << LOGN);
     constexpr int threads = (1 << LOGN) / EPT;
-    ntt_pass_kernel<FWD, true, true, LOGN, 1, 1, EPT, Job><<<grid, threads, 0, st>>>(d, job, 0, jbase);
+    ntt_pass_kernel<FWD, true, true, LOGN, 1, 1, EPT, LOGN, 0, Job><<<grid, threads, 0, st>>>(d, job, jbase);
     note_launch();
 }
 
@@ -501,11 +500,15 @@ void launch_ntt_two(const Dev& d, const Job& job, int jbase, int njobs, cudaStre
     dim3 grid(n / NTT_TILE, njobs);
     note_launch(2);
     if constexpr (FWD) {
-        ntt_pass_kernel<true, true, false, LA, 1, CA, EA, Job><<<grid, NTT_TILE / EA, 0, st>>>(d, job, 0, jbase);
-        ntt_pass_kernel<true, false, true, LB, HB, 1, EB, Job><<<grid, NTT_TILE / EB, 0, st>>>(d, job, LA, jbase);
+        ntt_pass_kernel<true, true, false, LA, 1, CA, EA, LA + LB, 0, Job>
+            <<<grid, NTT_TILE / EA, 0, st>>>(d, job, jbase);
+        ntt_pass_kernel<true, false, true, LB, HB, 1, EB, LA + LB, LA, Job>
+            <<<grid, NTT_TILE / EB, 0, st>>>(d, job, jbase);
     } else {
-        ntt_pass_kernel<false, true, false, LB, HB, 1, EB, Job><<<grid, NTT_TILE / EB, 0, st>>>(d, job, LA, jbase);
-        ntt_pass_kernel<false, false, true, LA, 1, CA, EA, Job><<<grid, NTT_TILE / EA, 0, st>>>(d, job, 0, jbase);
+        ntt_pass_kernel<false, true, false, LB, HB, 1, EB, LA + LB, LA, Job>
+            <<<grid, NTT_TILE / EB, 0, st>>>(d, job, jbase);
+        ntt_pass_kernel<false, false, true, LA, 1, CA, EA, LA + LB, 0, Job>
+            <<<grid, NTT_TILE / EA, 0, st>>>(d, job, jbase);
     }
 }
 

@@ -478,8 +478,8 @@ static void launch_modup_inner(const Dev& d, int B, int l, u64* D, u64* E, const
     const int njobs = B * (l + 1) * (l + 1);
     for (int base = 0; base < njobs; base += 65535) {
         const int cnt = njobs - base < 65535 ? njobs - base : 65535;
-        ntt_pass_kernel<true, true, false, LA, 1, CA, NTT_EPT16, JobModUp>
-            <<<dim3(n / NTT_TILE, cnt), NTT_TILE / NTT_EPT16, 0, st>>>(d, job, 0, base);
+        ntt_pass_kernel<true, true, false, LA, 1, CA, NTT_EPT16, LA + LB, 0, JobModUp>
+            <<<dim3(n / NTT_TILE, cnt), NTT_TILE / NTT_EPT16, 0, st>>>(d, job, base);
         note_launch();
     }
     // HS_MODUP_MINB=1 trades occupancy for registers (A/B knob for profiling)

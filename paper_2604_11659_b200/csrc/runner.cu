@@ -102,6 +102,13 @@ struct DeviceArena {
 // hs_keygen_register).  Generated keys live in a fixed pool of `cap` key
 // buffers; generation runs on a side stream so the next batch's keys are
 // produced while the current batch computes (events order reuse).
+// HS_KEYGEN_NO_PREFETCH=1: generate each batch's keys only when it needs
+// them (A/B knob for the side-stream overlap).
+static bool prefetch_on() {
+    static const bool off = getenv("HS_KEYGEN_NO_PREFETCH") != nullptr;
+    return !off;
+}
+
 struct KeyProvider {
     hs_ctx* c;
     cudaStream_t st;
@@ -112,12 +119,8 @@ struct KeyProvider {
     int64_t clock = 0;
 
     ~KeyProvider() {
+        // buffers, events and the side stream belong to the context (reused)
         if (side) cudaStreamSynchronize(side);
-        cudaStreamSynchronize(st);
-        for (u64* b : buf) cudaFree(b);
-        for (auto e : gen_ev) cudaEventDestroy(e);
-        for (auto e : use_ev) cudaEventDestroy(e);
-        if (side) cudaStreamDestroy(side);
     }
     bool resident(u32 r) const { return c->galois.count(r) != 0; }
     int slot_of(u32 r) const {
@@ -128,18 +131,24 @@ struct KeyProvider {
     bool needs_generation(u32 r) const { return !resident(r) && slot_of(r) < 0; }
     hs_status init(int cap) {
         if (!buf.empty() || cap <= 0) return HS_OK;
-        HS_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-        buf.assign(cap, nullptr);
-        tag.assign(cap, -1);
-        last.assign(cap, 0);
-        gen_ev.resize(cap);
-        use_ev.resize(cap);
-        for (int k = 0; k < cap; k++) {
-            HS_CUDA(cudaMalloc((void**)&buf[k], c->key_bytes()));
-            HS_CUDA(cudaEventCreateWithFlags(&gen_ev[k], cudaEventDisableTiming));
-            HS_CUDA(cudaEventCreateWithFlags(&use_ev[k], cudaEventDisableTiming));
-            HS_CUDA(cudaEventRecord(use_ev[k], st));
+        if (!c->kpool_side) HS_CUDA(cudaStreamCreateWithFlags(&c->kpool_side, cudaStreamNonBlocking));
+        side = c->kpool_side;
+        while ((int)c->kpool_buf.size() < cap) {
+            u64* b = nullptr;
+            cudaEvent_t g, u;
+            HS_CUDA(cudaMalloc((void**)&b, c->key_bytes()));
+            HS_CUDA(cudaEventCreateWithFlags(&g, cudaEventDisableTiming));
+            HS_CUDA(cudaEventCreateWithFlags(&u, cudaEventDisableTiming));
+            c->kpool_buf.push_back(b);
+            c->kpool_gen_ev.push_back(g);
+            c->kpool_use_ev.push_back(u);
         }
+        buf.assign(c->kpool_buf.begin(), c->kpool_buf.begin() + cap);
+        gen_ev.assign(c->kpool_gen_ev.begin(), c->kpool_gen_ev.begin() + cap);
+        use_ev.assign(c->kpool_use_ev.begin(), c->kpool_use_ev.begin() + cap);
+        tag.assign(cap, -1);                 // contents are regenerated every call
+        last.assign(cap, 0);
+        for (int k = 0; k < cap; k++) HS_CUDA(cudaEventRecord(use_ev[k], st));
         return HS_OK;
     }
     // Start generating the missing keys of `steps` on the side stream, never
@@ -383,7 +392,7 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, cons
             std::vector<const u64*> kp;
             hs_status ks_ = KP.acquire(chunk, kp);
             if (ks_ != HS_OK) return ks_;
-            if (any_gen && r0 + rc < R) {      // next chunk's keys while this one computes
+            if (any_gen && r0 + rc < R && prefetch_on()) {   // next chunk's keys while this one computes
                 const int rn = std::min<int>((int)rmax, R - r0 - rc);
                 ks_ = KP.prefetch(std::vector<u32>(steps_src.begin() + r0 + rc,
                                                    steps_src.begin() + r0 + rc + rn), chunk);
@@ -462,7 +471,7 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, cons
         std::vector<const u64*> bkeys;
         hs_status ks_ = KP.acquire(bsteps, bkeys);
         if (ks_ != HS_OK) return ks_;
-        if (lazy_needed && bi + 2 < bstart.size()) {
+        if (lazy_needed && bi + 2 < bstart.size() && prefetch_on()) {
             ks_ = KP.prefetch(bsteps_all[bi + 1], bsteps);
             if (ks_ != HS_OK) return ks_;
         }
