@@ -151,7 +151,7 @@ struct SrcPlain {      // x = ct(b).poly[i]
     HS_DEV B bind(int b, int i, int l, u32 n, const Dev&) const {
         return B{ct.at(b) + ((size_t)poly * (l + 1) + i) * n};
     }
-    HS_DEV u64 x(const B& s, u32 j, const Dev&, const PrimeConst&) const { return s.x[j]; }
+    HS_DEV u64 x(const B& s, u32 j, const Dev&, const PrimeConst&) const { return __ldg(s.x + j); }
 };
 struct SrcPerm {       // x = automorphism_g(ct(b).c1)[i]
     ItemPtr ct;
@@ -164,7 +164,7 @@ struct SrcPerm {       // x = automorphism_g(ct(b).c1)[i]
         return B{ct.at(b) + ((size_t)(l + 1) + i) * n, gal[b]};
     }
     HS_DEV u64 x(const B& s, u32 j, const Dev& d, const PrimeConst&) const {
-        return s.x[galois_perm(j, s.g, d.log_n)];
+        return __ldg(s.x + galois_perm(j, s.g, d.log_n));
     }
 };
 struct SrcTensor {     // x = d2 = a1 * b1 of the tensor product of two cts
@@ -178,7 +178,7 @@ struct SrcTensor {     // x = d2 = a1 * b1 of the tensor product of two cts
         return B{a.at(b) + o, bb.at(b) + o};
     }
     HS_DEV u64 x(const B& s, u32 j, const Dev&, const PrimeConst& P) const {
-        return mul_mod(s.a[j], s.b[j], P);
+        return mul_mod(__ldg(s.a + j), __ldg(s.b + j), P);
     }
 };
 
@@ -239,7 +239,7 @@ struct JobModUp {                           // forward NTT, job = (b*(l+1)+i)*(l
     }
     HS_DEV int prime(const Ctx& c) const { return c.pm; }
     HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst& P) const {
-        return lift_mod_sel(c.d[j], c.qsrc, P, c.small);
+        return lift_mod_sel(__ldg(c.d + j), c.qsrc, P, c.small);
     }
     HS_DEV u64* scratch(const Ctx& c) const { return c.e; }
     HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst& P) const { c.e[j] = canon4(v, P); }
@@ -321,11 +321,11 @@ struct AddTensor {     // relinearize after mult_ct: d0 = a0 b0, d1 = a0 b1 + a1
         return B{A + o0, A + o1, Bp + o0, Bp + o1, poly};
     }
     HS_DEV u64 v(const B& s, u32 j, const Dev&, const PrimeConst& P) const {
-        const u64 a0 = s.a0[j], b0 = s.b0[j];
+        const u64 a0 = __ldg(s.a0 + j), b0 = __ldg(s.b0 + j);
         if (s.poly == 0) return mul_mod(a0, b0, P);
         u64 lo = 0, hi = 0;
-        mac128(lo, hi, a0, s.b1[j]);
-        mac128(lo, hi, s.a1[j], b0);
+        mac128(lo, hi, a0, __ldg(s.b1 + j));
+        mac128(lo, hi, __ldg(s.a1 + j), b0);
         return barrett128(lo, hi, P);
     }
 };
@@ -337,7 +337,7 @@ struct AddPoly {       // d0/d1 taken from a stored ct (npoly polys at level l)
     HS_DEV B bind(int b, int poly, int m, int l, const Dev& d) const {
         return B{ct.at(b) + ((size_t)poly * (l + 1) + m) * d.n};
     }
-    HS_DEV u64 v(const B& s, u32 j, const Dev&, const PrimeConst&) const { return s.p[j]; }
+    HS_DEV u64 v(const B& s, u32 j, const Dev&, const PrimeConst&) const { return __ldg(s.p + j); }
 };
 struct AddPermC0 {     // rotation: automorphism_g(c0) on poly 0
     ItemPtr ct;
@@ -350,7 +350,7 @@ struct AddPermC0 {     // rotation: automorphism_g(c0) on poly 0
         return B{poly ? nullptr : ct.at(b) + (size_t)m * d.n, poly ? 0u : gal[b]};
     }
     HS_DEV u64 v(const B& s, u32 j, const Dev& d, const PrimeConst&) const {
-        return s.c0 ? s.c0[galois_perm(j, s.g, d.log_n)] : 0ull;
+        return s.c0 ? __ldg(s.c0 + galois_perm(j, s.g, d.log_n)) : 0ull;
     }
 };
 
@@ -380,12 +380,12 @@ struct JobModDown {                          // forward NTT, job = (b*2+c)*(l+1)
     }
     HS_DEV int prime(const Ctx& c) const { return c.m; }
     HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst& P) const {
-        return lift_mod_sel(c.t[j], d.aux_q, P, c.small);
+        return lift_mod_sel(__ldg(c.t + j), d.aux_q, P, c.small);
     }
     HS_DEV u64* scratch(const Ctx& c) const { return c.out; }
     HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst& P) const {
         // (acc - v) p^-1 + addend, one canonicalisation: acc < q, v < 4q
-        const u64 r = shoup_lazy(c.acc[j] + (P.two_q << 1) - v, c.w.x, c.w.y, P.q);   // [0, 2q)
+        const u64 r = shoup_lazy(__ldg(c.acc + j) + (P.two_q << 1) - v, c.w.x, c.w.y, P.q);   // [0, 2q)
         c.out[j] = csub(csub(r + add.v(c.add, j, d, P), P.two_q), P.q);
     }
 };
@@ -596,12 +596,12 @@ struct JobRescale {                          // forward NTT, job = (b*npoly+c)*l
     }
     HS_DEV int prime(const Ctx& c) const { return c.i; }
     HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst& P) const {
-        return lift_mod_sel(c.t[j], c.ql, P, c.small);
+        return lift_mod_sel(__ldg(c.t + j), c.ql, P, c.small);
     }
     HS_DEV u64* scratch(const Ctx& c) const { return c.out; }
     HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst& P) const {
-        u64 r = shoup_lazy(c.x[j] + (P.two_q << 1) - v, c.w.x, c.w.y, P.q);            // [0, 2q)
-        if (c.mask) r = mont_mul_lazy(r, c.mask[j], P.q, P.qinv_neg);                 // [0, 2q)
+        u64 r = shoup_lazy(__ldg(c.x + j) + (P.two_q << 1) - v, c.w.x, c.w.y, P.q);    // [0, 2q)
+        if (c.mask) r = mont_mul_lazy(r, __ldg(c.mask + j), P.q, P.qinv_neg);         // [0, 2q)
         c.out[j] = csub(r, P.q);
     }
 };
