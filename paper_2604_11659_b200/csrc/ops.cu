@@ -126,7 +126,7 @@ struct JobInvGather {
         return Ctx{in.at(b) + ((size_t)poly * nl + limb) * n, dst + (size_t)jb * n};
     }
     HS_DEV int prime(const Ctx&) const { return prime_idx; }
-    HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst&) const { return c.src[j]; }
+    HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst&) const { return __ldg(c.src + j); }
     HS_DEV u64* scratch(const Ctx& c) const { return c.dst; }
     HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst& P) const {
         c.dst[j] = shoup(v, P.n_inv, P.n_inv_sh, P.q);
