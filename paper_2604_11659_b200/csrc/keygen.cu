@@ -582,6 +582,113 @@ __global__ void __launch_bounds__(RNG_T) pk_uniform_fused(ParArgs A, int digit, 
 }
 
 
+// All L+2 uniform segments of one digit in ONE cooperative launch: CTA
+// (tile, key) stays resident and walks the segments in order.  A segment's
+// start position is published by the CTA that wrote its predecessor's n-th
+// value (tagged word: tag << 40 | position); within a segment the tiles use
+// the same decoupled look-back as pk_uniform_fused.  Flags and start words
+// have one slot per (key, segment[, tile]): tiles past a segment's end can lag
+// arbitrarily far behind without their slots being overwritten.  Saves ~L+1
+// launches per digit and the launch-to-launch drain (dominant at K ~ 20).
+HS_DEV unsigned long long ld_relaxed(const unsigned long long* p) {
+    unsigned long long x;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(x) : "l"(p) : "memory");
+    return x;
+}
+
+__global__ void __launch_bounds__(RNG_T) pk_uniform_persist(ParArgs A, int digit, int kbase,
+                                                            unsigned long long* flags,
+                                                            unsigned long long* segpos, u32 seq0) {
+    __shared__ U128 s_x;
+    __shared__ u32 cnt[RNG_E * RNG_W];
+    __shared__ u32 s_total, s_prefix;
+    __shared__ u64 s_pos;
+    const int k = kbase + (int)blockIdx.y, tile = blockIdx.x;
+    const u32 t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const u32 n = A.n;
+    const KeyStream ks = A.streams[k];
+    const U128 inc{ks.inc_hi, ks.inc_lo};
+    const U128 AT = A.jump->A[RNG_T], CT = mul128(A.jump->S[RNG_T], inc);
+    const int nseg = A.L + 2;
+    unsigned long long* sp = segpos + (size_t)k * nseg;       // [nseg] start words
+    const bool spec = (u64)tile * RNG_CH >= n;
+    for (int m = 0; m < nseg; m++) {
+        const u32 seq = seq0 + (u32)m;
+        unsigned long long* fl = flags + ((size_t)k * nseg + m) * A.NT;
+        if (t == 0) {
+            u64 p;
+            if (m == 0) {
+                p = A.pos_in[k];
+            } else {
+                unsigned long long x;
+                do {
+                    x = ld_relaxed(sp + m);
+                } while ((u32)(x >> 40) != seq);
+                p = x & ((1ull << 40) - 1ull);
+            }
+            s_pos = p;
+        }
+        __syncthreads();
+        const u64 pos = s_pos;
+        bool skip = false;
+        if (spec) {
+            if (warp == 0) {
+                const u32 pf = look_back(fl, tile, seq);
+                if (lane == 0) s_prefix = pf;
+            }
+            __syncthreads();
+            skip = s_prefix >= n;
+            if (skip && t == 0) publish(fl + tile, seq, 0u);
+        }
+        if (!skip) {
+            U128 st = tile_state(A, ks, pos + (u64)tile * RNG_CH, &s_x);
+            const u64 q = A.pc[m].q, thr = A.thr[m];
+            u64 val[RNG_E];
+            unsigned ball[RNG_E];
+#pragma unroll
+            for (int e = 0; e < RNG_E; e++) {
+                const u64 x = xsl_rr(st);
+                st = add128(mul128(st, AT), CT);
+                val[e] = __umul64hi(x, q);
+                ball[e] = __ballot_sync(0xffffffffu, x * q >= thr);
+                if (lane == 0) cnt[e * RNG_W + warp] = __popc(ball[e]);
+            }
+            const u32 total = chunk_scan(cnt, &s_total);
+            if (t == 0) publish(fl + tile, seq, total);
+            if (!spec) {
+                if (warp == 0) {
+                    const u32 pf = look_back(fl, tile, seq);
+                    if (lane == 0) s_prefix = pf;
+                }
+                __syncthreads();
+            }
+            const u32 prefix = s_prefix;
+            if (t == 0 && tile == A.NT - 1 && prefix + total < n) *A.err = 1;
+            if (prefix < n) {
+                u64* dst = A.a_out[k] + ((size_t)digit * (A.L + 2) + m) * n;
+#pragma unroll
+                for (int e = 0; e < RNG_E; e++) {
+                    if (!((ball[e] >> lane) & 1u)) continue;
+                    const u32 idx = prefix + cnt[e * RNG_W + warp] + __popc(ball[e] & lt);
+                    if (idx < n) dst[idx] = val[e];
+                    if (idx == n - 1) {
+                        const u64 next = pos + (u64)tile * RNG_CH + e * RNG_T + t + 1;
+                        if (m + 1 < nseg) {
+                            asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(sp + m + 1),
+                                         "l"(((unsigned long long)(seq + 1) << 40) | next)
+                                         : "memory");
+                        } else {
+                            A.pos_out[k] = next;
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();            // shared state is reused by the next segment
+    }
+}
+
 // Normal segment token parse, one CTA per key, everything in shared memory:
 //  1. every non-fast position s is evaluated as if it started a token:
 //     layer zs != 0 -> accept bit from the exp test with draw s+1 (2 draws);
@@ -872,9 +979,21 @@ size_t keygen_par_window(u32 n) {
     return (w + RNG_CH - 1) / RNG_CH * RNG_CH;
 }
 
+static size_t keygen_par_scratch_core(int K, u32 n) {
+    const size_t W = keygen_par_window(n), NT = W / RNG_CH;
+    return (size_t)K * (W * 8 + W * 8 + W * 4 + W / 32 * 4 * 2 + NT * 4 + NT * 8) + (size_t)K * 16;
+}
+
+// flags [K][L+2][NT] and start words [K][L+2] of the persistent uniform kernel
+// (L+2 <= 64 primes bounds the size; the layout only needs K, n and L).
+static size_t keygen_persist_scratch(int K, u32 n) {
+    const size_t W = keygen_par_window(n), NT = W / RNG_CH;
+    return (size_t)K * 64 * (NT + 1) * 8;
+}
+
 size_t keygen_par_scratch_bytes(int K, u32 n) {
     const size_t W = keygen_par_window(n), NT = W / RNG_CH;
-    return (size_t)K * (W * 8 + W * 8 + W * 4 + W / 32 * 4 * 2 + NT * 4 + NT * 8) + (size_t)K * 16 + 128;
+    return keygen_par_scratch_core(K, n) + keygen_persist_scratch(K, n) + 128;
 }
 
 // Replays K key streams in lockstep.  Returns false (nothing guaranteed) if
@@ -907,7 +1026,25 @@ void keygen_streams_parallel(const Dev& d, int K, const void* streams, u64* cons
     p += (size_t)2 * K * 8;
     unsigned long long* flags = (unsigned long long*)p;     // [K][NT] look-back flags
     cudaMemsetAsync(flags, 0, (size_t)K * NT * 8, st);
+    p += (size_t)K * NT * 8;
+    const int nseg = d.L + 2;
+    unsigned long long* pflags = (unsigned long long*)p;    // [K][L+2][NT] persistent look-back
+    p += (size_t)K * nseg * NT * 8;
+    unsigned long long* segpos = (unsigned long long*)p;    // [K][L+2] published segment starts
+    cudaMemsetAsync(pflags, 0, (size_t)K * nseg * (NT + 1) * 8, st);
     u32 seq = 0;
+    // keys per cooperative launch of the persistent uniform kernel (all its
+    // CTAs must be co-resident); 0 = use one launch per segment
+    static int coresident = -1;          // CTAs of pk_uniform_persist that fit at once
+    if (coresident < 0) {
+        int dev = 0, nsm = 0, per = 0, coop = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, pk_uniform_persist, RNG_T, 0);
+        coresident = (coop && !getenv("HS_KEYGEN_NO_PERSIST")) ? per * nsm : 0;
+    }
+    const int kgroup = coresident / NT;
     cudaMemsetAsync(pos[0], 0, (size_t)K * sizeof(u64), st);
     A.a_out = a_out;
     A.e_out = e_out;
@@ -921,12 +1058,28 @@ void keygen_streams_parallel(const Dev& d, int K, const void* streams, u64* cons
     const size_t walk_smem = (size_t)5 * (W / 32) * sizeof(unsigned);
     cudaFuncSetAttribute(pk_normal_walk2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)walk_smem);
     for (int digit = 0; digit <= d.L; digit++) {
-        for (int m = 0; m < d.L + 2; m++) {
+        if (kgroup > 0) {
             A.pos_in = pos[cur];
             A.pos_out = pos[cur ^ 1];
-            pk_uniform_fused<<<grid, RNG_T, 0, st>>>(A, digit, m, flags, ++seq);
-            note_launch();
+            const u32 seq0 = seq + 1;
+            for (int k0 = 0; k0 < K; k0 += kgroup) {
+                const int kc = std::min(kgroup, K - k0);
+                int dg = digit, kb = k0;
+                u32 s0 = seq0;
+                void* args[] = {&A, &dg, &kb, &pflags, &segpos, &s0};
+                cudaLaunchCooperativeKernel((void*)pk_uniform_persist, dim3(NT, kc), dim3(RNG_T), args, 0, st);
+                note_launch();
+            }
+            seq += d.L + 2;
             cur ^= 1;
+        } else {
+            for (int m = 0; m < d.L + 2; m++) {
+                A.pos_in = pos[cur];
+                A.pos_out = pos[cur ^ 1];
+                pk_uniform_fused<<<grid, RNG_T, 0, st>>>(A, digit, m, flags, ++seq);
+                note_launch();
+                cur ^= 1;
+            }
         }
         A.pos_in = pos[cur];
         A.pos_out = pos[cur ^ 1];
