@@ -302,3 +302,52 @@ def test_runner_missing_key_and_layout_errors(pkg):
         engine.spmm_csr_csc(ea, eb, ctx, keys)
     with pytest.raises(ParameterError, match="layout mismatch"):
         engine.spmm_csr_csc(eb, ea, ctx, keys)
+
+
+def test_bench_workload_full_size(pkg, oracle_mod):
+    """The bench workload itself (BASELINE configs[1]: N = 2^14, L = 2,
+    64 x 64 @ 75%, 16,434 pairs, 4,773 device-generated keys): the full product
+    decrypts to the plaintext product, a sampled sub-schedule is bit-identical
+    to the CPU oracle, and disjoint shards of the full schedule sum to the
+    full result (size-independent properties at full size)."""
+    import torch
+    import bench
+    from paper_2604_11659_b200 import device as D
+    from paper_2604_11659_b200 import encmat, engine
+    from paper_2604_11659_b200._lib import check, lib
+    O = oracle_mod
+    wl = dict(bench.WORKLOADS["cfg2"])
+    params = pkg.build_params(wl["ring_degree"], wl["scale_bits"], wl["levels"], wl["seed"])
+    ctx = pkg.CkksContext(params)
+    keys = ctx.keygen()
+    from paper_2604_11659_b200 import formats
+    seed = bench.cell_seed(wl["dim"])
+    a = formats.generate_random_sparse(wl["dim"], wl["sparsity"], (seed, 0))
+    b = formats.generate_random_sparse(wl["dim"], wl["sparsity"], (seed, 1))
+    ea = encmat.encrypt_sparse(a, encmat.Layout.CSR, ctx, keys)
+    eb = encmat.encrypt_sparse(b, encmat.Layout.CSC, ctx, keys)
+    keys = ctx.gen_galois_keys(encmat.required_rotation_steps(ea.meta, eb.meta), keys, device=True)
+    pairs = encmat.pair_array(ea.meta, eb.meta)
+    assert len(pairs) == 16434
+    mc = engine.MaskCache(ctx, wl["dim"])
+    mc.prewarm(np.unique(np.minimum(pairs[:, 2], pairs[:, 3])))
+    full = engine.spmm_csr_csc(ea, eb, ctx, keys, engine.OpCounter(), mc)
+    err = O.frobenius_error(encmat.decrypt_result(full, ctx, keys), O.plain_matmul(a, b))
+    assert err < 1e-6, err
+    # shards of the full schedule sum to the full result
+    parts = []
+    for r in range(3):
+        res = engine.run_pairs(ea, eb, ctx, keys, engine.OpCounter(), mc, None, shard=(r, 3))
+        parts.append(res.ctxt.data.view(torch.int64).clone())
+    summed = torch.stack(parts).sum(0)
+    check(lib().hs_reduce_mod(ctx.handle, D.ptr(summed), 2, params.levels - 1, D.stream()))
+    assert np.array_equal(D.to_host(summed.view(torch.uint64)), _arr(full.ctxt))
+    # a sampled sub-schedule vs the oracle on identical inputs
+    sub = pairs[:: len(pairs) // 48][:48]
+    res = engine.run_pairs(ea, eb, ctx, keys, engine.OpCounter(), mc, sub)
+    octx = O.OracleContext(O.build_params(wl["ring_degree"], wl["scale_bits"], wl["levels"], wl["seed"]))
+    okeys = octx.keygen()
+    octx.gen_galois_keys(O.rotation_steps(sub.tolist(), wl["dim"]), okeys)
+    masks = {int(p): np.stack(mc.get(int(p)).limbs) for p in np.unique(np.minimum(sub[:, 2], sub[:, 3]))}
+    want = octx.spmspm(_arr(ea.ctxt), _arr(eb.ctxt), sub, wl["dim"], masks, okeys)
+    assert np.array_equal(_arr(res.ctxt), want)
