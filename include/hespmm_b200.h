@@ -157,6 +157,10 @@ hs_status hs_encrypt(hs_ctx* ctx, const int64_t* v, const int64_t* e0, const int
 /* pt[i] = c0[i] + c1[i] s[i] (context.py:303-313) */
 hs_status hs_decrypt(hs_ctx* ctx, const uint64_t* ct, const uint64_t* sk, uint32_t level,
                      uint64_t* pt, void* stream);
+/* Exact centred CRT lift of nl coefficient-domain limbs [nl][n] (device) to
+ * float64 (device, n): Garner + big-integer centring + round-half-even, the
+ * doubles bit-equal to the reference's big-int decode (context.py:244-279). */
+hs_status hs_crt_decode(hs_ctx* ctx, const uint64_t* coeff, int32_t nlimbs, double* out, void* stream);
 /* Convert limbs to / from Montgomery form in place (masks are kept that way). */
 hs_status hs_to_montgomery(hs_ctx* ctx, uint64_t* data, int32_t nitems, int32_t nlimbs,
                            int32_t prime_first, int32_t inverse, void* stream);

@@ -47,6 +47,7 @@ _SIGS = {
     "hs_keygen_set_tables": (ctypes.c_int, [c_vp, ctypes.POINTER(ctypes.c_double),
                                             ctypes.POINTER(ctypes.c_double), c_u64p]),
     "hs_keygen_set_secret": (ctypes.c_int, [c_vp, c_vp, c_vp]),
+    "hs_crt_decode": (ctypes.c_int, [c_vp, c_vp, ctypes.c_int32, c_vp, c_vp]),
     "hs_key_generate_galois": (ctypes.c_int, [c_vp, ctypes.POINTER(ctypes.c_uint32), c_u64p,
                                               ctypes.c_int32, c_vp]),
     "hs_keygen_register": (ctypes.c_int, [c_vp, ctypes.POINTER(ctypes.c_uint32), c_u64p,

@@ -292,7 +292,17 @@ class CkksContext:
         return out
 
     def _crt_to_float(self, limbs: torch.Tensor) -> np.ndarray:
-        """Exact centred CRT lift of the coefficients, as float64 (context.py:244-279)."""
+        """Exact centred CRT lift of the coefficients, as float64 (context.py:244-279),
+        on the device (csrc/decode.cu: Garner + round-half-even, bit-equal to
+        the reference's Python big-int path kept below as ``_crt_to_float_host``)."""
+        nl = limbs.shape[0]
+        coeff = self._intt_copy(limbs, nl)
+        out = torch.empty(self._n, dtype=torch.float64, device=coeff.device)
+        check(lib().hs_crt_decode(self._h, D.ptr(coeff), nl, out.data_ptr(), D.stream()))
+        return out.cpu().numpy()
+
+    def _crt_to_float_host(self, limbs: torch.Tensor) -> np.ndarray:
+        """The reference's big-integer decode restated on the host (test oracle)."""
         nl = limbs.shape[0]
         coeff = D.to_host(self._intt_copy(limbs, nl))
         if nl == 1:

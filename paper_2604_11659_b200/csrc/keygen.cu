@@ -992,7 +992,6 @@ static size_t keygen_persist_scratch(int K, u32 n) {
 }
 
 size_t keygen_par_scratch_bytes(int K, u32 n) {
-    const size_t W = keygen_par_window(n), NT = W / RNG_CH;
     return keygen_par_scratch_core(K, n) + keygen_persist_scratch(K, n) + 128;
 }
 

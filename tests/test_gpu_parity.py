@@ -351,3 +351,35 @@ def test_bench_workload_full_size(pkg, oracle_mod):
     masks = {int(p): np.stack(mc.get(int(p)).limbs) for p in np.unique(np.minimum(sub[:, 2], sub[:, 3]))}
     want = octx.spmspm(_arr(ea.ctxt), _arr(eb.ctxt), sub, wl["dim"], masks, okeys)
     assert np.array_equal(_arr(res.ctxt), want)
+
+
+@pytest.mark.parametrize("n,sb,L", [(1024, 45, 2), (16384, 50, 2), (8192, 45, 4), (65536, 50, 24)])
+def test_device_crt_decode_bit_equal_to_big_int(pkg, n, sb, L):
+    """csrc/decode.cu vs the reference's big-integer decode restated on the
+    host, on random limbs at every level (incl. values near +-Q/2)."""
+    import torch
+    from paper_2604_11659_b200 import device as D
+    params = pkg.build_params(n, sb, L, 2024)
+    ctx = pkg.CkksContext(params)
+    rng = np.random.default_rng(n + L)
+    import random
+    pyr = random.Random(n + L)
+    for nl in sorted({1, 2, L + 1}):
+        qs = [int(q) for q in params.modulus_chain[:nl]]
+        Q = 1
+        for q in qs:
+            Q *= q
+        # signed values up to 2^min(bits(Q)-2, 1000) (float() of larger ones overflows
+        # in the reference too), plus the centring boundary when Q is small enough
+        bits = min(Q.bit_length() - 2, 1000)
+        xs = [pyr.randrange(-(1 << bits), 1 << bits) >> pyr.randrange(0, bits) for _ in range(n)]
+        if Q.bit_length() < 1020:
+            xs[:5] = [(Q - 1) // 2, -((Q - 1) // 2), 0, -1, 1]
+        limbs = np.array([[x % q for x in xs] for q in qs], dtype=np.uint64)
+        t = D.to_dev(limbs)
+        # both paths INTT internally: feed NTT-domain limbs
+        from paper_2604_11659_b200._lib import check, lib
+        check(lib().hs_ntt(ctx.handle, D.ptr(t), 1, nl, 0, 0, D.stream()))
+        got = ctx._crt_to_float(t)
+        want = ctx._crt_to_float_host(t)
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), nl
