@@ -383,3 +383,27 @@ def test_device_crt_decode_bit_equal_to_big_int(pkg, n, sb, L):
         got = ctx._crt_to_float(t)
         want = ctx._crt_to_float_host(t)
         assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), nl
+
+
+def test_distributed_path_single_rank_nccl(pkg):
+    """The multi-GPU code path (dist.spmm_csr_csc_distributed: shard, NCCL
+    int64 SUM, mod-q kernel) on a one-rank NCCL group equals the runner."""
+    import os
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_2604_11659_b200 import dist as hdist
+    from paper_2604_11659_b200 import engine
+    params, ctx, keys, a, b, ea, eb, full, counter, mc = product_runner_case(
+        pkg, 1024, 45, 2, 2024, 8, 0.5, 3)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        res = hdist.spmm_csr_csc_distributed(ea, eb, ctx, keys, engine.OpCounter(), mc)
+        assert np.array_equal(_arr(res.ctxt), _arr(full.ctxt))
+        assert res.ctxt.scale == full.ctxt.scale and res.ctxt.level == full.ctxt.level
+    finally:
+        dist.destroy_process_group()
