@@ -41,6 +41,7 @@ sys.path.insert(0, ROOT)
 
 WORKLOADS = {
     "cfg2": dict(ring_degree=1 << 14, scale_bits=50, levels=2, seed=2024, dim=64, sparsity=0.75,
+                 batch_gb=24,       # runner work budget (keys 15 GB + 24 GB work on 180 GB HBM)
                  desc="configs[1]: N=2^14, 64x64 @75% sparsity, single B200"),
     "cfg1": dict(ring_degree=1 << 10, scale_bits=45, levels=2, seed=2024, dim=16, sparsity=0.5,
                  desc="configs[0]: desk-small params (pkg/params), 16x16 @50%"),
