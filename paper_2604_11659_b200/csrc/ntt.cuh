@@ -296,6 +296,14 @@ HS_DEV void unit_butterflies(u64* v, const ulonglong2* __restrict__ tw, u32 Y, u
 // [0, 4q) in both directions.  Internal invariants: forward LZ values grow
 // by < 4q per stage from < 4q; forward Harvey values stay in [0, 8q) (csub
 // by 4q, approximate Shoup in [0, 4q)); inverse values stay in [0, 4q).
+// Unroll factor of the staged (coalesced, one element per step) load/store
+// loops: these inline the job's loader/epilogue, so full unrolling of 16
+// copies of a heavy epilogue costs instruction-cache misses.
+#ifndef NTT_IO_UNROLL
+#define NTT_IO_UNROLL 4            // A/B at cfg2: 16 -> 174.0 ms, 4 -> 167.5, 2 -> 171.0
+#endif
+constexpr int kIoUnroll = NTT_IO_UNROLL;   // (#pragma arguments are not macro-expanded)
+
 // LOGN (log2 ring degree) and S0 (first stage of the pass) are template
 // parameters so every index shift/mask below is a compile-time constant.
 template <bool FWD, bool FIRST, bool LAST, int LOGG, int H, int C, int EPT, int LOGN, int S0, class Job>
@@ -402,7 +410,7 @@ struct PassEngine {
             }
         } else {
             u64* buf = sm;                // "exchange 0": exchange I uses buffer I & 1
-#pragma unroll
+#pragma unroll kIoUnroll
             for (int k = 0; k < EPT; k++) {
                 const u32 i = E.t + k * T;
                 buf[spad16(i)] = in(job, E, E.gidx(i / (G * C), (i / C) % G, i % C));
@@ -426,7 +434,7 @@ struct PassEngine {
             u64* buf = sm + (NR & 1) * SMW;   // the buffer not written by the last exchange
             scatter<RLAST>(buf, v, E);
             __syncthreads();
-#pragma unroll
+#pragma unroll kIoUnroll
             for (int k = 0; k < EPT; k++) {
                 const u32 i = E.t + k * T;
                 out<LZ>(job, E, E.gidx(i / (G * C), (i / C) % G, i % C), buf[spad16(i)]);
