@@ -303,6 +303,11 @@ HS_DEV void unit_butterflies(u64* v, const ulonglong2* __restrict__ tw, u32 Y, u
 #define NTT_IO_UNROLL 4            // A/B at cfg2: 16 -> 174.0 ms, 4 -> 167.5, 2 -> 171.0
 #endif
 constexpr int kIoUnroll = NTT_IO_UNROLL;   // (#pragma arguments are not macro-expanded)
+// 1: a pass whose loader is the job's (FIRST) always stages its tile through
+// shared memory (rolled loop: smaller code) instead of loading directly.
+#ifndef NTT_STAGED_FIRST
+#define NTT_STAGED_FIRST 0
+#endif
 
 // LOGN (log2 ring degree) and S0 (first stage of the pass) are template
 // parameters so every index shift/mask below is a compile-time constant.
@@ -399,7 +404,7 @@ struct PassEngine {
         using MF = RM<RFIRST>;
         using ML = RM<RLAST>;
         // ---- load
-        if constexpr (MF::direct) {
+        if constexpr (MF::direct && !(FIRST && NTT_STAGED_FIRST)) {
             constexpr u32 gstride = 1u << (MF::LOWB + LO_BITS);
 #pragma unroll
             for (int k = 0; k < MF::UPT; k++) {
