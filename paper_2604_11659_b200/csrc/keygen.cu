@@ -1183,14 +1183,15 @@ struct JobKeyFused {
     HS_DEV int prime(const Ctx& c) const { return c.m; }
     HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst& P) const {
         const long long v = __ldg(c.e + j);
-        if (v >= 0) return reduce64((u64)v, P);
-        const u64 t = reduce64((u64)(-(v + 1)) + 1ull, P);
-        return t ? P.q - t : 0ull;
+        const bool neg = v < 0;                               // |v| mod q, then negate: one path
+        const u64 t = reduce64(neg ? (u64)(-(v + 1)) + 1ull : (u64)v, P);
+        return (neg && t) ? P.q - t : t;
     }
     HS_DEV u64* scratch(const Ctx& c) const { return c.b; }
     HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst& P) const {
         u64 acc = csub(csub(v, P.two_q), P.q);
-        if (c.m <= L) acc = add_mod(acc, shoup(__ldg(c.skpm + j), c.f.x, c.f.y, P.q), P.q);
+        // f = 0 for the aux modulus (m = L+1): one code path
+        acc = add_mod(acc, shoup(__ldg(c.skpm + j), c.f.x, c.f.y, P.q), P.q);
         // a * sk with sk's Shoup companion (stored after the L+2 sk limbs)
         const u64 ask = csub(shoup_lazy(__ldg(c.a + j), __ldg(c.skm + j), __ldg(c.skm + (size_t)(L + 2) * d.n + j), P.q), P.q);
         c.b[j] = sub_mod(acc, ask, P.q);

@@ -310,22 +310,22 @@ struct AddNone {
 };
 struct AddTensor {     // relinearize after mult_ct: d0 = a0 b0, d1 = a0 b1 + a1 b0
     ItemPtr a, bb;
+    // one code path for both polys: x0 y0 + x1 y1 with (x1, y1) absent for d0
+    // (the inlined epilogue is instruction-cache bound, not ALU bound)
     struct B {
-        const u64 *a0, *a1, *b0, *b1;
-        int poly;
+        const u64 *x0, *y0, *x1, *y1;
     };
     HS_DEV B bind(int b, int poly, int m, int l, const Dev& d) const {
         const u64* A = a.at(b);
         const u64* Bp = bb.at(b);
         const size_t o0 = (size_t)m * d.n, o1 = ((size_t)(l + 1) + m) * d.n;
-        return B{A + o0, A + o1, Bp + o0, Bp + o1, poly};
+        return poly ? B{A + o0, Bp + o1, A + o1, Bp + o0} : B{A + o0, Bp + o0, nullptr, nullptr};
     }
     HS_DEV u64 v(const B& s, u32 j, const Dev&, const PrimeConst& P) const {
-        const u64 a0 = __ldg(s.a0 + j), b0 = __ldg(s.b0 + j);
-        if (s.poly == 0) return mul_mod(a0, b0, P);
         u64 lo = 0, hi = 0;
-        mac128(lo, hi, a0, __ldg(s.b1 + j));
-        mac128(lo, hi, __ldg(s.a1 + j), b0);
+        mac128(lo, hi, __ldg(s.x0 + j), __ldg(s.y0 + j));
+        const u64 x1 = s.x1 ? __ldg(s.x1 + j) : 0ull, y1 = s.x1 ? __ldg(s.y1 + j) : 0ull;
+        mac128(lo, hi, x1, y1);
         return barrett128(lo, hi, P);
     }
 };
@@ -601,7 +601,9 @@ struct JobRescale {                          // forward NTT, job = (b*npoly+c)*l
     HS_DEV u64* scratch(const Ctx& c) const { return c.out; }
     HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst& P) const {
         u64 r = shoup_lazy(__ldg(c.x + j) + (P.two_q << 1) - v, c.w.x, c.w.y, P.q);    // [0, 2q)
-        if (c.mask) r = mont_mul_lazy(r, __ldg(c.mask + j), P.q, P.qinv_neg);         // [0, 2q)
+        // mask in Montgomery form; no mask = Montgomery one (2^64 mod q): one code path
+        const u64 mk = c.mask ? __ldg(c.mask + j) : P.r_mod;
+        r = mont_mul_lazy(r, mk, P.q, P.qinv_neg);                                    // [0, 2q)
         c.out[j] = csub(r, P.q);
     }
 };
