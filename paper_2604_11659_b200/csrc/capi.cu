@@ -149,8 +149,9 @@ hs_status hs_ctx_create(hs_ctx** out, int device, uint32_t n, uint32_t levels,
     c->primes.assign(chain, chain + L + 1);
     c->primes.push_back(aux);
     for (u64 q : c->primes) {
-        if (q >= (1ull << 61) || q < 3 || (q - 1) % (2ull * n) || !is_prime_u64(q)) {
-            set_error("non-NTT-friendly prime " + std::to_string(q));
+        // < 2^60: the kernels keep lazy residues in [0, 8q) and test signs (8q < 2^63)
+        if (q >= (1ull << 60) || q < 3 || (q - 1) % (2ull * n) || !is_prime_u64(q)) {
+            set_error("non-NTT-friendly prime (or >= 2^60) " + std::to_string(q));
             delete c;
             return (hs_status)HS_PARAMETER_ERROR;
         }
@@ -433,7 +434,7 @@ hs_status hs_signed_to_ntt(hs_ctx* c, const int64_t* coeffs, int32_t nlimbs, int
 
 hs_status hs_seam_op(int32_t op, uint64_t count, const uint64_t* a, const uint64_t* b, uint64_t* out,
                      uint64_t q, uint64_t s, uint64_t q_src, void* stream) {
-    if (op < 0 || op > SEAM_EXTEND || q < 3 || q >= (1ull << 61)) {
+    if (op < 0 || op > SEAM_EXTEND || q < 3 || q >= (1ull << 60)) {
         set_error("bad seam op or modulus");
         return (hs_status)HS_PARAMETER_ERROR;
     }
@@ -461,6 +462,10 @@ hs_status hs_seam_ntt(uint64_t* a, uint32_t n, uint64_t q, const uint64_t* roots
                       const uint64_t* roots_sh, uint64_t n_inv, int32_t inverse, void* stream) {
     if (n < 8 || (n & (n - 1)) || n > (1u << 17)) {
         set_error("bad ring degree");
+        return (hs_status)HS_PARAMETER_ERROR;
+    }
+    if (q < 3 || q >= (1ull << 60)) {
+        set_error("bad modulus (the kernels need q < 2^60)");
         return (hs_status)HS_PARAMETER_ERROR;
     }
     // Tables are rebuilt per call from the caller's arrays (the seam is for API

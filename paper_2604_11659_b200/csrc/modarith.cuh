@@ -30,7 +30,13 @@ struct PrimeConst {
 
 HS_DEV u64 mulhi64(u64 a, u64 b) { return __umul64hi(a, b); }
 
-HS_DEV u64 csub(u64 x, u64 m) { return x >= m ? x - m : x; }
+// x - m if x >= m.  Every value the kernels reduce is < 8q < 2^63 (all
+// primes < 2^60), so the sign of x - m decides (one compare fewer than an
+// unsigned 64-bit >=).
+HS_DEV u64 csub(u64 x, u64 m) {
+    const u64 d = x - m;
+    return (long long)d < 0 ? x : d;
+}
 
 // Shoup product, w_sh = floor(w*2^64/q).  Any x < 2^64; result in [0, 2q).
 HS_DEV u64 shoup_lazy(u64 x, u64 w, u64 w_sh, u64 q) {
