@@ -303,6 +303,11 @@ HS_DEV void unit_butterflies(u64* v, const ulonglong2* __restrict__ tw, u32 Y, u
 #define NTT_IO_UNROLL 4            // A/B at cfg2: 16 -> 174.0 ms, 4 -> 167.5, 2 -> 171.0
 #endif
 constexpr int kIoUnroll = NTT_IO_UNROLL;   // (#pragma arguments are not macro-expanded)
+// 1: rounds with two units per thread run them as a rolled loop (one copy of
+// the butterfly code + register swaps).
+#ifndef NTT_ROLL_UNITS
+#define NTT_ROLL_UNITS 0
+#endif
 // 1: a pass whose loader is the job's (FIRST) always stages its tile through
 // shared memory (rolled loop: smaller code) instead of loading directly.
 #ifndef NTT_STAGED_FIRST
@@ -375,11 +380,28 @@ struct PassEngine {
     template <int r, bool LZ>
     HS_DEV static void compute(u64* v, const Env& E) {
         using M = RM<r>;
+        if constexpr (NTT_ROLL_UNITS && M::UPT == 2) {
+            // two units of NU: one copy of the butterfly code, the halves
+            // swapped between iterations (code size over a few moves)
+#pragma unroll 1
+            for (int k = 0; k < 2; k++) {
+                const auto u = M::unit(E.t + k * T);
+                const u32 Y = (((1u << S0) + E.hi0 + u.h) << M::AA) + u.gh;
+                unit_butterflies<FWD, LZ, M::RR>(v, E.tw, Y, E.nq, E.P.two_q, E.four_q);
 #pragma unroll
-        for (int k = 0; k < M::UPT; k++) {
-            const auto u = M::unit(E.t + k * T);
-            const u32 Y = (((1u << S0) + E.hi0 + u.h) << M::AA) + u.gh;
-            unit_butterflies<FWD, LZ, M::RR>(v + k * M::NU, E.tw, Y, E.nq, E.P.two_q, E.four_q);
+                for (int e = 0; e < M::NU; e++) {
+                    const u64 x = v[e];
+                    v[e] = v[M::NU + e];
+                    v[M::NU + e] = x;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < M::UPT; k++) {
+                const auto u = M::unit(E.t + k * T);
+                const u32 Y = (((1u << S0) + E.hi0 + u.h) << M::AA) + u.gh;
+                unit_butterflies<FWD, LZ, M::RR>(v + k * M::NU, E.tw, Y, E.nq, E.P.two_q, E.four_q);
+            }
         }
     }
 
