@@ -54,8 +54,9 @@ HS_DEV u64 redc128_std(u64 lo, u64 hi, const PrimeConst& P) {
 // lo mod q (Barrett), one exact canonical result.  Cheaper than REDC + the
 // Montgomery correction (redc128_std) for standard-form keys.
 HS_DEV u64 reduce128(u64 lo, u64 hi, const PrimeConst& P) {
-    const u64 t = shoup_lazy(hi, P.r_mod, P.r_sh, P.q) + reduce64(lo, P);     // < 3q
-    return csub(csub(t, P.two_q), P.q);
+    // approximate quotients (ntt.cuh): each part in [0, 4q), sum < 8q
+    const u64 t = shoup_ax(hi, P.r_mod, P.r_sh, 0ull - P.q) + reduce64_lazy(lo, P);
+    return csub(csub(csub(t, P.two_q << 1), P.two_q), P.q);
 }
 
 // Barrett reduction of a 128-bit value x < 2 q^2 (same estimate as mul_mod).
