@@ -93,12 +93,8 @@ HS_DEV u64 shoup_ax(u64 x, u64 w, u64 w_sh, u64 nq) {
     return r;
 }
 
-// Forward passes run fully lazy ("LZ") when every intermediate stays far
-// below 2^63: inputs < 4q, each of <= 17 stages adds < 4q (approximate Shoup),
-// so values stay < 72q < 2^63 for q < 2^56 (the ~50-bit chain primes).  The
-// 60-bit q_0 and aux prime keep Harvey's [0, 4q) butterflies.  Lazy outputs
-// reach a job's store() in [0, 4q) via reduce64_lazy (any t < 2^64).
-HS_DEV bool fwd_lazy_ok(const PrimeConst& P) { return P.q < (1ull << 56); }
+// t mod q up to a small multiple: [0, 4q) for any t < 2^64 (approximate
+// Barrett quotient with floor(2^64 / q)).
 HS_DEV u64 reduce64_lazy(u64 t, const PrimeConst& P) { return t - mulhi_apx(t, P.m64) * P.q; }
 
 // ======================================================= radix-8 smem rounds
@@ -261,7 +257,7 @@ struct RoundMap {
 // Butterflies of one unit (2^R values in v[]).  Twiddle of local stage j,
 // element e: tw[(Y << j) + (e >> (R - j))] with Y = ((2^s0 + hi) << A) + gh,
 // i.e. roots[m + block] of the reference loop (_fast.pyx:55-66).
-template <bool FWD, bool LZ, int R>
+template <bool FWD, int R>
 HS_DEV void unit_butterflies(u64* v, const ulonglong2* __restrict__ tw, u32 Y, u64 nq, u64 two_q,
                              u64 four_q) {
     constexpr int NU = 1 << R;
@@ -275,8 +271,7 @@ HS_DEV void unit_butterflies(u64* v, const ulonglong2* __restrict__ tw, u32 Y, u
             if (e & bit) continue;
             const ulonglong2 w = twp[e >> (R - j)];
             if (FWD) {
-                // LZ: x unbounded-lazy (grows < 4q per stage); else [0, 8q) -> [0, 4q)
-                const u64 x = LZ ? v[e] : csub_s(v[e], four_q);
+                const u64 x = csub_s(v[e], four_q);                        // [0, 8q) -> [0, 4q)
                 const u64 t = shoup_ax(v[e + bit], w.x, w.y, nq);          // [0, 4q)
                 v[e] = x + t;
                 v[e + bit] = x - t + four_q;
@@ -293,9 +288,9 @@ HS_DEV void unit_butterflies(u64* v, const ulonglong2* __restrict__ tw, u32 Y, u
 // CTA (pointer-table lookups, index decoding), then prime(ctx),
 // load(ctx, j, P), scratch(ctx), store(ctx, j, v, P) per element.  load()
 // returns [0, q) (forward loads may return up to 4q); store() receives
-// [0, 4q) in both directions.  Internal invariants: forward LZ values grow
-// by < 4q per stage from < 4q; forward Harvey values stay in [0, 8q) (csub
-// by 4q, approximate Shoup in [0, 4q)); inverse values stay in [0, 4q).
+// [0, 4q) in both directions.  Internal invariants: forward (Harvey) values
+// stay in [0, 8q) (csub by 4q, approximate Shoup in [0, 4q)); inverse values
+// stay in [0, 4q).
 // Unroll factor of the staged (coalesced, one element per step) load/store
 // loops: these inline the job's loader/epilogue, so full unrolling of 16
 // copies of a heavy epilogue costs instruction-cache misses.
@@ -345,10 +340,9 @@ struct PassEngine {
         if constexpr (FIRST) return job.load(E.jc, j, E.P);
         else return job.scratch(E.jc)[j];
     }
-    template <bool LZ>
     HS_DEV static void out(const Job& job, const Env& E, u32 j, u64 v) {
         if constexpr (LAST) {
-            if (FWD) v = LZ ? reduce64_lazy(v, E.P) : csub_s(v, E.four_q);
+            if (FWD) v = csub_s(v, E.four_q);                          // [0, 8q) -> [0, 4q)
             job.store(E.jc, j, v, E.P);
         } else {
             job.scratch(E.jc)[j] = v;
@@ -377,7 +371,7 @@ struct PassEngine {
             for (int e = 0; e < M::NU; e++) p[M::off(e)] = v[k * M::NU + e];
         }
     }
-    template <int r, bool LZ>
+    template <int r>
     HS_DEV static void compute(u64* v, const Env& E) {
         using M = RM<r>;
         if constexpr (NTT_ROLL_UNITS && M::UPT == 2) {
@@ -387,7 +381,7 @@ struct PassEngine {
             for (int k = 0; k < 2; k++) {
                 const auto u = M::unit(E.t + k * T);
                 const u32 Y = (((1u << S0) + E.hi0 + u.h) << M::AA) + u.gh;
-                unit_butterflies<FWD, LZ, M::RR>(v, E.tw, Y, E.nq, E.P.two_q, E.four_q);
+                unit_butterflies<FWD, M::RR>(v, E.tw, Y, E.nq, E.P.two_q, E.four_q);
 #pragma unroll
                 for (int e = 0; e < M::NU; e++) {
                     const u64 x = v[e];
@@ -400,13 +394,13 @@ struct PassEngine {
             for (int k = 0; k < M::UPT; k++) {
                 const auto u = M::unit(E.t + k * T);
                 const u32 Y = (((1u << S0) + E.hi0 + u.h) << M::AA) + u.gh;
-                unit_butterflies<FWD, LZ, M::RR>(v + k * M::NU, E.tw, Y, E.nq, E.P.two_q, E.four_q);
+                unit_butterflies<FWD, M::RR>(v + k * M::NU, E.tw, Y, E.nq, E.P.two_q, E.four_q);
             }
         }
     }
 
     // rounds after the first, in execution order (I = 1 .. NR-1)
-    template <int I, bool LZ>
+    template <int I>
     HS_DEV static void rest(u64* sm, u64* v, const Env& E) {
         if constexpr (I < NR) {
             constexpr int rp = FWD ? I - 1 : NR - I;        // previous round
@@ -415,12 +409,11 @@ struct PassEngine {
             scatter<rp>(buf, v, E);
             __syncthreads();
             gather<r>(buf, v, E);
-            compute<r, LZ>(v, E);
-            rest<I + 1, LZ>(sm, v, E);
+            compute<r>(v, E);
+            rest<I + 1>(sm, v, E);
         }
     }
 
-    template <bool LZ>
     HS_DEV static void run(u64* sm, const Env& E, const Job& job) {
         u64 v[EPT];
         using MF = RM<RFIRST>;
@@ -445,8 +438,8 @@ struct PassEngine {
             __syncthreads();
             gather<RFIRST>(buf, v, E);
         }
-        compute<RFIRST, LZ>(v, E);
-        rest<1, LZ>(sm, v, E);
+        compute<RFIRST>(v, E);
+        rest<1>(sm, v, E);
         // ---- store
         if constexpr (ML::direct) {
             constexpr u32 gstride = 1u << (ML::LOWB + LO_BITS);
@@ -455,7 +448,7 @@ struct PassEngine {
                 const auto u = ML::unit(E.t + k * T);
                 const u32 j0 = E.gidx(u.h, u.g, u.c);
 #pragma unroll
-                for (int e = 0; e < ML::NU; e++) out<LZ>(job, E, j0 + e * gstride, v[k * ML::NU + e]);
+                for (int e = 0; e < ML::NU; e++) out(job, E, j0 + e * gstride, v[k * ML::NU + e]);
             }
         } else {
             u64* buf = sm + (NR & 1) * SMW;   // the buffer not written by the last exchange
@@ -464,7 +457,7 @@ struct PassEngine {
 #pragma unroll kIoUnroll
             for (int k = 0; k < EPT; k++) {
                 const u32 i = E.t + k * T;
-                out<LZ>(job, E, E.gidx(i / (G * C), (i / C) % G, i % C), buf[spad16(i)]);
+                out(job, E, E.gidx(i / (G * C), (i / C) % G, i % C), buf[spad16(i)]);
             }
         }
     }
@@ -493,11 +486,11 @@ ntt_pass_kernel(Dev d, Job job, int jbase) {
     E.t = threadIdx.x;
     E.nq = 0ull - E.P.q;
     E.four_q = E.P.two_q << 1;
-    // One code path for every prime: the lazy forward variant (run<true>,
-    // no upper-input reduction for sub-2^56 primes) saves ~5 instructions per
-    // butterfly but doubles the kernel's code, and instruction-cache misses
-    // cost more than that (A/B on B200: 194.9 vs 206.7 ms per cfg2 matmul).
-    PE::template run<false>(sm, E, job);
+    // One code path for every prime: a lazy forward variant (no upper-input
+    // reduction for sub-2^56 primes) saved ~5 instructions per butterfly but
+    // doubled the kernel's code, and instruction-cache misses cost more than
+    // that (A/B on B200: 194.9 vs 206.7 ms per cfg2 matmul).
+    PE::run(sm, E, job);
 }
 
 // Single-pass variant for small limbs (whole limb in one CTA, 8 per thread).
