@@ -1,3 +1,4 @@
+#include <algorithm>
 // Device operations of the encrypted SpMSpM path: limb kernels, key
 // switching (decompose -> ModUp -> key inner product -> ModDown), rescale,
 // tensor product, NTT-domain Galois automorphism, accumulation.
@@ -681,23 +682,60 @@ void add_batch(const Dev& d, int B, int l, int npoly, ItemPtr a, ItemPtr b, Item
     note_launch();
 }
 
-__global__ void accum_kernel(Dev d, int B, int nl, ItemPtr src, u64* acc) {
+// Order-free modular sum over items, in two stages so that
+// the item loop is split over CTAs: stage 1 writes one partial per chunk of
+// items (grid.z = chunks), stage 2 folds the partials into acc.  (One CTA
+// column per limb walking all B items serially left the GPU idle at level 0.)
+__global__ void accum_partial_kernel(Dev d, int B, int nl, int chunk, ItemPtr src, u64* part,
+                                     bool accumulate_into) {
     const u32 n = d.n;
     const u32 k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const int m = blockIdx.y % nl;
     const u64 q = d.pc[m].q;
     const size_t o = (size_t)blockIdx.y * n + k;
+    const int b0 = blockIdx.z * chunk, b1 = min(B, b0 + chunk);
+    u64* dst = part + (size_t)blockIdx.z * gridDim.y * n + o;
+    u64 s = accumulate_into ? *dst : 0ull;
+    for (int b = b0; b < b1; b++) s = add_mod(s, __ldg(src.at(b) + o), q);
+    *dst = s;
+}
+
+__global__ void accum_fold_kernel(Dev d, int nl, int nchunks, const u64* part, u64* acc) {
+    const u32 n = d.n;
+    const u32 k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int m = blockIdx.y % nl;
+    const u64 q = d.pc[m].q;
+    const size_t o = (size_t)blockIdx.y * n + k, stride = (size_t)gridDim.y * n;
     u64 s = acc[o];
-    for (int b = 0; b < B; b++) s = add_mod(s, src.at(b)[o], q);
+    for (int c = 0; c < nchunks; c++) s = add_mod(s, part[c * stride + o], q);
     acc[o] = s;
 }
 
 void accumulate(const Dev& d, int B, int nl, int npoly, ItemPtr src, u64* acc, cudaStream_t st) {
     if (B <= 0) return;
-    dim3 g((d.n + 255) / 256, npoly * nl);
-    accum_kernel<<<g, 256, 0, st>>>(d, B, nl, src, acc);
-    note_launch();
+    const int limbs = npoly * nl;
+    const int cols = (int)((d.n + 255) / 256) * limbs;
+    // enough CTAs for ~8 per SM, chunks of >= 16 items
+    int nchunks = std::max(1, std::min((B + 15) / 16, (148 * 8 + cols - 1) / cols));
+    const int chunk = (B + nchunks - 1) / nchunks;
+    nchunks = (B + chunk - 1) / chunk;
+    u64* part = nullptr;
+    if (cudaMallocAsync((void**)&part, (size_t)nchunks * limbs * d.n * sizeof(u64), st) != cudaSuccess) {
+        cudaGetLastError();
+        part = nullptr;
+    }
+    if (!part) {                                   // no scratch: one chunk straight into acc
+        accum_partial_kernel<<<dim3((d.n + 255) / 256, limbs, 1), 256, 0, st>>>(d, B, nl, B, src, acc, true);
+        note_launch();
+        return;
+    }
+    accum_partial_kernel<<<dim3((d.n + 255) / 256, limbs, nchunks), 256, 0, st>>>(d, B, nl, chunk, src, part,
+                                                                                  false);
+    accum_fold_kernel<<<dim3((d.n + 255) / 256, limbs), 256, 0, st>>>(d, nl, nchunks, part, acc);
+    note_launch(2);
+    cudaFreeAsync(part, st);
 }
 
 __global__ void mont_kernel(Dev d, u64* buf, size_t total, PrimeMap pm, bool inverse) {
