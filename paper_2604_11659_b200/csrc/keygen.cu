@@ -590,13 +590,16 @@ __global__ void __launch_bounds__(RNG_T) pk_uniform_fused(ParArgs A, int digit, 
 // have one slot per (key, segment[, tile]): tiles past a segment's end can lag
 // arbitrarily far behind without their slots being overwritten.  Saves ~L+1
 // launches per digit and the launch-to-launch drain (dominant at K ~ 20).
+#ifndef KG_PERSIST_MINB
+#define KG_PERSIST_MINB 3      // (A/B: 3 -> 1.16 ms/key vs 2 -> 1.26 at K=23) co-resident CTAs per SM (keys per cooperative launch = that x 148 / tiles)
+#endif
 HS_DEV unsigned long long ld_relaxed(const unsigned long long* p) {
     unsigned long long x;
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(x) : "l"(p) : "memory");
     return x;
 }
 
-__global__ void __launch_bounds__(RNG_T) pk_uniform_persist(ParArgs A, int digit, int kbase,
+__global__ void __launch_bounds__(RNG_T, KG_PERSIST_MINB) pk_uniform_persist(ParArgs A, int digit, int kbase,
                                                             unsigned long long* flags,
                                                             unsigned long long* segpos, u32 seq0) {
     __shared__ U128 s_x;
