@@ -182,7 +182,9 @@ hs_status hs_ctx_create(hs_ctx** out, int device, uint32_t n, uint32_t levels,
         }
     }
     // key-switch and rescale constants (reference context.py:39-53)
-    std::vector<ulonglong2> df(L + 1), auxinv(L + 1), qlinv((size_t)(L + 1) * (L + 1));
+    // df: [L+1] digit factors, then [L+1] digit factors times 2^64 (for a
+    // Montgomery-form digit source, csrc/ops.cu SrcTensor)
+    std::vector<ulonglong2> df(2 * (L + 1)), auxinv(L + 1), qlinv((size_t)(L + 1) * (L + 1));
     c->df.resize(L + 1);
     c->auxinv.resize(L + 1);
     c->qlinv.assign((size_t)(L + 1) * (L + 1), 0);
@@ -192,6 +194,7 @@ hs_status hs_ctx_create(hs_ctx** out, int device, uint32_t n, uint32_t levels,
             if (j != i) prod = (u64)((u128)prod * (c->primes[j] % qi) % qi);
         c->df[i] = invmod(prod, qi);
         df[i] = shoup_pair(c->df[i], qi);
+        df[L + 1 + i] = shoup_pair((u64)(((u128)c->df[i] << 64) % qi), qi);
         c->auxinv[i] = invmod(aux % qi, qi);
         auxinv[i] = shoup_pair(c->auxinv[i], qi);
     }
@@ -237,6 +240,7 @@ hs_status hs_ctx_create(hs_ctx** out, int device, uint32_t n, uint32_t levels,
     d.tw = (const ulonglong2*)(base + off_tw);
     d.itw = (const ulonglong2*)(base + off_itw);
     d.df = (const ulonglong2*)(base + off_df);
+    d.dfR = d.df + (L + 1);
     d.auxinv = (const ulonglong2*)(base + off_ai);
     d.qlinv = (const ulonglong2*)(base + off_ql);
     *out = c;

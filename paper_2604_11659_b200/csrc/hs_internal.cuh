@@ -21,6 +21,7 @@ struct Dev {
     const ulonglong2* tw;        // [(L+2) * n] {w, floor(w 2^64 / q)} forward roots
     const ulonglong2* itw;       // inverse roots
     const ulonglong2* df;        // [L+1] digit factor (Q_L/q_i)^-1 mod q_i, Shoup pair
+    const ulonglong2* dfR;       // [L+1] the same times 2^64 mod q_i
     const ulonglong2* auxinv;    // [L+1] p^-1 mod q_m
     const ulonglong2* qlinv;     // [(L+1)*(L+1)] q_lvl^-1 mod q_i at [lvl*(L+1)+i]
 };

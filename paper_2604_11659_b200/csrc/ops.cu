@@ -170,6 +170,9 @@ struct SrcPerm {       // x = automorphism_g(ct(b).c1)[i]
     }
 };
 struct SrcTensor {     // x = d2 = a1 * b1 of the tensor product of two cts
+    // Montgomery product a1 b1 2^-64 (cheaper than Barrett); the 2^64 is
+    // folded into the digit factor the decomposition applies next (dfR).
+    static constexpr bool kMont = true;
     ItemPtr a, bb;
     struct B {
         const u64* a;
@@ -180,9 +183,14 @@ struct SrcTensor {     // x = d2 = a1 * b1 of the tensor product of two cts
         return B{a.at(b) + o, bb.at(b) + o};
     }
     HS_DEV u64 x(const B& s, u32 j, const Dev&, const PrimeConst& P) const {
-        return mul_mod(__ldg(s.a + j), __ldg(s.b + j), P);
+        return mont_mul_lazy(__ldg(s.a + j), __ldg(s.b + j), P.q, P.qinv_neg);    // [0, 2q)
     }
 };
+
+template <class S, class = void>
+struct SrcMont { static constexpr bool value = false; };
+template <class S>
+struct SrcMont<S, std::void_t<decltype(S::kMont)>> { static constexpr bool value = S::kMont; };
 
 template <class Src>
 struct JobDecompose {                       // inverse NTT, job = b*(l+1)+i
@@ -203,7 +211,7 @@ struct JobDecompose {                       // inverse NTT, job = b*(l+1)+i
     HS_DEV Ctx make(int jb) const {
         const int b = jb / (l + 1), i = jb % (l + 1);
         return Ctx{src.bind(b, i, l, n, d), E + ((size_t)jb * (l + 2) + i) * n, D + (size_t)jb * n,
-                   df[i], i};
+                   SrcMont<Src>::value ? d.dfR[i] : df[i], i};
     }
     HS_DEV int prime(const Ctx& c) const { return c.i; }
     HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst& P) const {
