@@ -263,6 +263,10 @@ struct JobModUp {                           // forward NTT, job = (b*(l+1)+i)*(l
 // adjacent coefficients so key rows move as 16-byte loads and more loads are
 // in flight per thread.  grid = (ceil(n/512), l+2, B).
 constexpr int KSI_T = 256;
+#ifndef KSI_UNROLL
+#define KSI_UNROLL 2
+#endif
+constexpr int kKsiUnroll = KSI_UNROLL;
 
 __global__ void __launch_bounds__(KSI_T, 4)
 ks_inner_kernel(Dev d, int l, const u64* __restrict__ E, size_t e_item_stride,
@@ -286,7 +290,7 @@ ks_inner_kernel(Dev d, int l, const u64* __restrict__ E, size_t e_item_stride,
         (const ulonglong2*)(key + (size_t)(d.L + 1) * kstride + (size_t)pm * n + k);
     const size_t kst2 = kstride / 2;
     u64 lb0 = 0, hb0 = 0, la0 = 0, ha0 = 0, lb1 = 0, hb1 = 0, la1 = 0, ha1 = 0;
-#pragma unroll 2
+#pragma unroll kKsiUnroll
     for (int i = 0; i <= l; i++, Ei += estride, kb += kst2, ka += kst2) {
         u64 e0, e1;
         if (g) {
