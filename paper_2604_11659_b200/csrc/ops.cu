@@ -371,13 +371,14 @@ struct AddPermC0 {     // rotation: automorphism_g(c0) on poly 0
 };
 
 template <class Add>
-struct JobModDown {                          // forward NTT, job = (b*2+c)*(l+1)+m
+struct JobModDown {                          // forward NTT, job = (b*2+c)*nm+(m-m0)
     const u64* T;
     const u64* ACC;
     ItemPtr out;                             // per item ct [2][l+1][n]
     Add add;
     int l;
     Dev d;
+    int m0, nm;                              // limbs m0 .. m0+nm-1 (all: 0, l+1)
     struct Ctx {
         const u64* t;        // INTT of the aux accumulator (coefficients mod p)
         const u64* acc;      // ACC[b][c][m]
@@ -388,7 +389,7 @@ struct JobModDown {                          // forward NTT, job = (b*2+c)*(l+1)
         bool small;          // p / 2 < q_m
     };
     HS_DEV Ctx make(int jb) const {
-        const int bc = jb / (l + 1), m = jb % (l + 1);
+        const int bc = jb / nm, m = m0 + jb % nm;
         const int b = bc >> 1, c = bc & 1;
         return Ctx{T + (size_t)bc * d.n, ACC + ((size_t)bc * (l + 2) + m) * d.n,
                    out.atw(b) + ((size_t)c * (l + 1) + m) * d.n, add.bind(b, c, m, l, d), d.auxinv[m], m,
@@ -421,7 +422,7 @@ static void mod_down(const Dev& d, int B, int l, const u64* ACC, u64* T, const A
     launch_ntt<false>(d, JobInvGather{strided(ACC, (size_t)(l + 2) * d.n), 1, l + 2, l + 1,
                                       d.L + 1, T, d.n},
                       B * 2, st);
-    launch_ntt<true>(d, JobModDown<Add>{T, ACC, out, add, l, d}, B * 2 * (l + 1), st);
+    launch_ntt<true>(d, JobModDown<Add>{T, ACC, out, add, l, d, 0, l + 1}, B * 2 * (l + 1), st);
 }
 
 // Fused ModUp second pass + key inner product.  One CTA owns a contiguous
@@ -559,6 +560,78 @@ void relin_batch(const Dev& d, int B, int l, ItemPtr ct3, const u64* const* keys
 void mult_relin_batch(const Dev& d, int B, int l, ItemPtr a, ItemPtr b, const u64* const* keys,
                       ItemPtr out, u64* scratch, cudaStream_t st) {
     key_switch_batch(d, B, l, SrcTensor{a, b}, AddTensor{a, b}, keys, out, scratch, st);
+}
+
+// ModDown followed by rescale, merged.  Both subtract the NTT of a lifted
+// coefficient vector and scale; the NTT mod q_m is linear, so for m < l
+//   out_m = (acc_m - NTT_m(lift_p T)) p^-1 + add_m                (ModDown)
+//   r_m   = (out_m - NTT_m(lift_ql u)) q_l^-1 mask_m,  u = INTT(out_l)
+//         = (acc_m p^-1 + add_m - NTT_m(lift_p(T) p^-1 + lift_ql(u))) q_l^-1 mask_m
+// -- exact modular identities, so r_m is the same residue the two separate
+// steps produce (hespmm/ckks/context.py key switch then rescale).  Only limb
+// l of the relinearised ct is formed; one forward NTT per (item, poly, m < l)
+// replaces two.
+template <class Add>
+struct JobModDownRescale {                   // forward NTT, job = (b*2+c)*l+m, m < l
+    const u64* T;                            // [bc][n] INTT of the aux accumulator (mod p)
+    const u64* U;                            // [bc][n] INTT of out limb l (mod q_l)
+    const u64* ACC;
+    ItemPtr out, mask;                       // out per item [2][l][n]; mask [l][n] (Montgomery)
+    Add add;
+    int l;
+    Dev d;
+    const ulonglong2* qlinv;                 // row for level l
+    struct Ctx {
+        const u64 *t, *u, *acc, *mask;
+        u64* out;
+        typename Add::B add;
+        ulonglong2 wp, wl;   // p^-1, q_l^-1 mod q_m
+        u64 ql;
+        int m;
+    };
+    HS_DEV Ctx make(int jb) const {
+        const int bc = jb / l, m = jb % l;
+        const int b = bc >> 1, c = bc & 1;
+        const bool has_mask = mask.tab || mask.base;
+        return Ctx{T + (size_t)bc * d.n, U + (size_t)bc * d.n, ACC + ((size_t)bc * (l + 2) + m) * d.n,
+                   has_mask ? mask.at(b) + (size_t)m * d.n : nullptr, out.atw(b) + ((size_t)c * l + m) * d.n,
+                   add.bind(b, c, m, l, d), d.auxinv[m], qlinv[m], d.pc[l].q, m};
+    }
+    HS_DEV int prime(const Ctx& c) const { return c.m; }
+    HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst& P) const {
+        const u64 tp = shoup_lazy(lift_mod(__ldg(c.t + j), d.aux_q, P), c.wp.x, c.wp.y, P.q);   // [0, 2q)
+        return tp + lift_mod(__ldg(c.u + j), c.ql, P);                                           // [0, 3q)
+    }
+    HS_DEV u64* scratch(const Ctx& c) const { return c.out; }
+    HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst& P) const {
+        const u64 y = shoup_lazy(__ldg(c.acc + j), c.wp.x, c.wp.y, P.q) + add.v(c.add, j, d, P);  // [0, 3q)
+        u64 r = shoup_lazy(y + (P.two_q << 1) - v, c.wl.x, c.wl.y, P.q);                         // [0, 2q)
+        const u64 mk = c.mask ? __ldg(c.mask + j) : P.r_mod;
+        r = mont_mul_lazy(r, mk, P.q, P.qinv_neg);                                               // [0, 2q)
+        c.out[j] = csub(r, P.q);
+    }
+};
+
+void mult_relin_rescale_batch(const Dev& d, int B, int l, ItemPtr a, ItemPtr b, const u64* const* keys,
+                              ItemPtr mask_mont, ItemPtr top, ItemPtr out, u64* scratch, u64* U,
+                              cudaStream_t st) {
+    const u32 n = d.n;
+    u64* E = scratch;
+    u64* D = E + (size_t)B * (l + 1) * (l + 2) * n;
+    u64* ACC = D + (size_t)B * (l + 1) * n;
+    u64* T = ACC + (size_t)B * 2 * (l + 2) * n;
+    const AddTensor add{a, b};
+    launch_ntt<false>(d, JobDecompose<SrcTensor>{SrcTensor{a, b}, E, D, d.df, l, n, d}, B * (l + 1), st);
+    modup_and_inner(d, B, l, D, E, keys, ACC, st);
+    launch_ntt<false>(d, JobInvGather{strided(ACC, (size_t)(l + 2) * n), 1, l + 2, l + 1, d.L + 1, T, n},
+                      B * 2, st);
+    // limb l of the relinearised ct (into top, ct layout [2][l+1][n]), then its INTT
+    launch_ntt<true>(d, JobModDown<AddTensor>{T, ACC, top, add, l, d, l, 1}, B * 2, st);
+    launch_ntt<false>(d, JobInvGather{top, 2, l + 1, l, l, U, n}, B * 2, st);
+    launch_ntt<true>(d,
+                     JobModDownRescale<AddTensor>{T, U, ACC, out, mask_mont, add, l, d,
+                                                  d.qlinv + (size_t)l * (d.L + 1)},
+                     B * 2 * l, st);
 }
 
 void rotate_batch(const Dev& d, int B, int l, ItemPtr ct, const u32* gal, const u64* const* keys,

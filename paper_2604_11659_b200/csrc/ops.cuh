@@ -46,6 +46,11 @@ void relin_batch(const Dev& d, int B, int l, ItemPtr ct3, const u64* const* keys
 // mult_ct fused with relinearize: out = relin(a (x) b) for B pairs at level l.
 void mult_relin_batch(const Dev& d, int B, int l, ItemPtr a, ItemPtr b, const u64* const* keys,
                       ItemPtr out, u64* scratch, cudaStream_t st);
+// mult_relin then rescale (with the mask product) of the result, merged:
+// out = rescale(relin(a * b)) * mask at level l-1; top receives limb l only.
+void mult_relin_rescale_batch(const Dev& d, int B, int l, ItemPtr a, ItemPtr b, const u64* const* keys,
+                              ItemPtr mask_mont, ItemPtr top, ItemPtr out, u64* scratch, u64* U,
+                              cudaStream_t st);
 // Rotation of B cts at level l by Galois elements gal[b] with keys[b].
 void rotate_batch(const Dev& d, int B, int l, ItemPtr ct, const u32* gal, const u64* const* keys,
                   ItemPtr out, u64* scratch, cudaStream_t st);

@@ -482,12 +482,20 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, cons
         HS_CUDA(cudaMemcpyAsync(dK + s, hK.data() + s, bn * sizeof(u64*), cudaMemcpyHostToDevice, st));
         int z = 0;
         while (z < bn && hG[s + z] == 0) z++;
-        // mult_ct + relinearize (fused), level L
-        mult_relin_batch(d, bn, L, table(dA + s), table(dB + s), dR, strided(Rb, (size_t)2 * (L + 1) * n),
-                         ks, st);
-        // rescale L -> L-1 fused with the mask product (mask in Montgomery form)
-        rescale_batch(d, bn, L, 2, strided(Rb, (size_t)2 * (L + 1) * n), strided(Mb, (size_t)2 * L * n),
-                      table(dM + s), Tb, st);
+        // mult_ct + relinearize, level L, then rescale L -> L-1 fused with the
+        // mask product (mask in Montgomery form)
+        static const bool split_mdr = getenv("HS_SPLIT_MODDOWN_RESCALE") != nullptr;
+        if (split_mdr) {
+            mult_relin_batch(d, bn, L, table(dA + s), table(dB + s), dR, strided(Rb, (size_t)2 * (L + 1) * n),
+                             ks, st);
+            rescale_batch(d, bn, L, 2, strided(Rb, (size_t)2 * (L + 1) * n), strided(Mb, (size_t)2 * L * n),
+                          table(dM + s), Tb, st);
+        } else {
+            // ModDown and the first rescale merged (ops.cu JobModDownRescale)
+            mult_relin_rescale_batch(d, bn, L, table(dA + s), table(dB + s), dR, table(dM + s),
+                                     strided(Rb, (size_t)2 * (L + 1) * n), strided(Mb, (size_t)2 * L * n), ks,
+                                     Tb, st);
+        }
         // relinearize of a degree-1 ct is a counted no-op (context.py:368-370)
         // rescale L-1 -> L-2
         rescale_batch(d, bn, L - 1, 2, strided(Mb, (size_t)2 * L * n), strided(Cb, ctL2),
