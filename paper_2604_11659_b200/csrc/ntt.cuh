@@ -257,7 +257,14 @@ struct RoundMap {
 // Butterflies of one unit (2^R values in v[]).  Twiddle of local stage j,
 // element e: tw[(Y << j) + (e >> (R - j))] with Y = ((2^s0 + hi) << A) + gh,
 // i.e. roots[m + block] of the reference loop (_fast.pyx:55-66).
-template <bool FWD, int R>
+// Forward values grow lazily (all primes are < 2^60, so 16q < 2^64): with
+// inputs in [0, 4q) and t = approximate Shoup product in [0, 4q), a stage
+// maps bound b to b + 4q, so stages 0-2 need no reduction (4q -> 16q); from
+// stage 3 on, every other stage first reduces the upper input by 8q
+// (16q -> 12q -> 16q ...).  GS = global index of the stage.
+HS_DEV constexpr bool fwd_reduce_at(int gs) { return gs >= 3 && ((gs - 3) & 1) == 0; }
+
+template <bool FWD, int R, int GS>
 HS_DEV void unit_butterflies(u64* v, const ulonglong2* __restrict__ tw, u32 Y, u64 nq, u64 two_q,
                              u64 four_q) {
     constexpr int NU = 1 << R;
@@ -271,7 +278,7 @@ HS_DEV void unit_butterflies(u64* v, const ulonglong2* __restrict__ tw, u32 Y, u
             if (e & bit) continue;
             const ulonglong2 w = twp[e >> (R - j)];
             if (FWD) {
-                const u64 x = csub_s(v[e], four_q);                        // [0, 8q) -> [0, 4q)
+                const u64 x = fwd_reduce_at(GS + jj) ? csub_s(v[e], four_q << 1) : v[e];   // < 12q
                 const u64 t = shoup_ax(v[e + bit], w.x, w.y, nq);          // [0, 4q)
                 v[e] = x + t;
                 v[e + bit] = x - t + four_q;
@@ -287,9 +294,10 @@ HS_DEV void unit_butterflies(u64* v, const ulonglong2* __restrict__ tw, u32 Y, u
 // Job interface: `typename Job::Ctx ctx = job.make(jb)` is evaluated once per
 // CTA (pointer-table lookups, index decoding), then prime(ctx),
 // load(ctx, j, P), scratch(ctx), store(ctx, j, v, P) per element.  load()
-// returns [0, q) (forward loads may return up to 4q); store() receives
+// returns [0, q) (forward loads may return < 4q); store() receives
 // [0, 4q) in both directions.  Internal invariants: forward (Harvey) values
-// stay in [0, 8q) (csub by 4q, approximate Shoup in [0, 4q)); inverse values
+// stay below 16q (fwd_reduce_at; forward loads must return < 4q, passes hand
+// raw values to the next pass), approximate Shoup in [0, 4q); inverse values
 // stay in [0, 4q).
 // Unroll factor of the staged (coalesced, one element per step) load/store
 // loops: these inline the job's loader/epilogue, so full unrolling of 16
@@ -342,7 +350,7 @@ struct PassEngine {
     }
     HS_DEV static void out(const Job& job, const Env& E, u32 j, u64 v) {
         if constexpr (LAST) {
-            if (FWD) v = csub_s(v, E.four_q);                          // [0, 8q) -> [0, 4q)
+            if (FWD) v = csub_s(csub_s(v, E.four_q << 1), E.four_q);   // [0, 16q) -> [0, 4q)
             job.store(E.jc, j, v, E.P);
         } else {
             job.scratch(E.jc)[j] = v;
@@ -381,7 +389,7 @@ struct PassEngine {
             for (int k = 0; k < 2; k++) {
                 const auto u = M::unit(E.t + k * T);
                 const u32 Y = (((1u << S0) + E.hi0 + u.h) << M::AA) + u.gh;
-                unit_butterflies<FWD, M::RR>(v, E.tw, Y, E.nq, E.P.two_q, E.four_q);
+                unit_butterflies<FWD, M::RR, S0 + M::AA>(v, E.tw, Y, E.nq, E.P.two_q, E.four_q);
 #pragma unroll
                 for (int e = 0; e < M::NU; e++) {
                     const u64 x = v[e];
@@ -394,7 +402,7 @@ struct PassEngine {
             for (int k = 0; k < M::UPT; k++) {
                 const auto u = M::unit(E.t + k * T);
                 const u32 Y = (((1u << S0) + E.hi0 + u.h) << M::AA) + u.gh;
-                unit_butterflies<FWD, M::RR>(v + k * M::NU, E.tw, Y, E.nq, E.P.two_q, E.four_q);
+                unit_butterflies<FWD, M::RR, S0 + M::AA>(v + k * M::NU, E.tw, Y, E.nq, E.P.two_q, E.four_q);
             }
         }
     }
