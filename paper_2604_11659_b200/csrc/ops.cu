@@ -639,6 +639,109 @@ void rotate_batch(const Dev& d, int B, int l, ItemPtr ct, const u32* gal, const 
     key_switch_batch(d, B, l, SrcPerm{ct, gal}, AddPermC0{ct, gal}, keys, out, scratch, st);
 }
 
+// Rotate B items and add them all into acc ([2][l+1][n]), with ONE ModDown
+// NTT per output limb instead of one per item.  ModDown of item b is
+//   out_b,m = (acc_b,m - NTT_m(lift_p T_b)) p^-1 + add_b,m
+// and the NTT mod q_m is linear, so
+//   sum_b out_b,m = (sum_b acc_b,m - NTT_m(sum_b lift_p T_b)) p^-1 + sum_b add_b,m
+// -- the same residues as rotating each item and adding (the reference's
+// per-item eval_rotate + eval_add, hespmm/engine.py accumulation loop).
+// rot_partial_kernel sums, per chunk of items, the coefficient/NTT vectors
+// F = [S0, S1, A0, A1, Z0, Z1] (acc per poly, addend per poly = permuted c0
+// and 0, lifted T per poly); accum_fold_kernel adds the chunks onto F, whose
+// A slots start as the running sum acc; JobRotAcc runs the NTT of Z and the
+// ModDown epilogue, overwriting acc (its scratch between the two passes).
+__global__ void __launch_bounds__(256)
+rot_partial_kernel(Dev d, int B, int l, int chunk, ItemPtr ct, const u32* __restrict__ gal,
+                   const u64* __restrict__ ACC, const u64* __restrict__ T, u64* __restrict__ part) {
+    const u32 n = d.n;
+    const u32 k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int m = blockIdx.y;
+    const PrimeConst P = d.pc[m];
+    const int b0 = blockIdx.z * chunk, b1 = min(B, b0 + chunk);
+    const size_t acc_item = (size_t)2 * (l + 2) * n;
+    u64 s0 = 0, s1 = 0, a0 = 0, z0 = 0, z1 = 0;
+    for (int b = b0; b < b1; b++) {
+        const u64* A = ACC + (size_t)b * acc_item + (size_t)m * n + k;
+        s0 = add_mod(s0, __ldg(A), P.q);
+        s1 = add_mod(s1, __ldg(A + (size_t)(l + 2) * n), P.q);
+        a0 = add_mod(a0, __ldg(ct.at(b) + (size_t)m * n + galois_perm(k, gal[b], d.log_n)), P.q);
+        z0 = add_mod(z0, lift_mod(__ldg(T + (size_t)b * 2 * n + k), d.aux_q, P), P.q);
+        z1 = add_mod(z1, lift_mod(__ldg(T + ((size_t)b * 2 + 1) * n + k), d.aux_q, P), P.q);
+    }
+    const size_t ls = (size_t)(l + 1) * n;              // one slot [l+1][n]
+    u64* dst = part + (size_t)blockIdx.z * 6 * ls + (size_t)m * n + k;
+    dst[0] = s0;
+    dst[ls] = s1;
+    dst[2 * ls] = a0;
+    dst[3 * ls] = 0ull;
+    dst[4 * ls] = z0;
+    dst[5 * ls] = z1;
+}
+
+struct JobRotAcc {                           // forward NTT, job = c*(l+1)+m
+    const u64* F;                            // [6][l+1][n] folded sums
+    u64* acc;                                // [2][l+1][n]
+    int l;
+    Dev d;
+    struct Ctx {
+        const u64 *z, *s, *a;
+        u64* out;
+        ulonglong2 w;        // p^-1 mod q_m
+        int m;
+    };
+    HS_DEV Ctx make(int jb) const {
+        const int c = jb / (l + 1), m = jb % (l + 1);
+        const size_t ls = (size_t)(l + 1) * d.n, o = (size_t)m * d.n;
+        return Ctx{F + (4 + c) * ls + o, F + c * ls + o, F + (2 + c) * ls + o, acc + (size_t)c * ls + o,
+                   d.auxinv[m], m};
+    }
+    HS_DEV int prime(const Ctx& c) const { return c.m; }
+    HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst&) const { return __ldg(c.z + j); }
+    HS_DEV u64* scratch(const Ctx& c) const { return c.out; }
+    HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst& P) const {
+        const u64 r = shoup_lazy(__ldg(c.s + j) + (P.two_q << 1) - v, c.w.x, c.w.y, P.q);   // [0, 2q)
+        c.out[j] = csub(csub(r + __ldg(c.a + j), P.two_q), P.q);
+    }
+};
+
+__global__ void accum_fold_kernel(Dev d, int nl, int nchunks, const u64* part, u64* acc);
+
+bool rotate_accumulate(const Dev& d, int B, int l, ItemPtr ct, const u32* gal, const u64* const* keys,
+                       u64* acc, u64* scratch, cudaStream_t st) {
+    const u32 n = d.n;
+    const int nl = l + 1;
+    const size_t ls = (size_t)nl * n;
+    // F and the chunk partials reuse the E region of the scratch (free after
+    // the inner product): room for F plus at least one chunk
+    const long cap = (long)((size_t)B * (l + 1) * (l + 2) * n / (6 * ls)) - 1;
+    if (B <= 0 || cap < 1) return false;
+    u64* E = scratch;
+    u64* D = E + (size_t)B * (l + 1) * (l + 2) * n;
+    u64* ACC = D + (size_t)B * (l + 1) * n;
+    u64* T = ACC + (size_t)B * 2 * (l + 2) * n;
+    launch_ntt<false>(d, JobDecompose<SrcPerm>{SrcPerm{ct, gal}, E, D, d.df, l, n, d}, B * (l + 1), st);
+    modup_and_inner(d, B, l, D, E, keys, ACC, st);
+    launch_ntt<false>(d, JobInvGather{strided(ACC, (size_t)(l + 2) * n), 1, l + 2, l + 1, d.L + 1, T, n},
+                      B * 2, st);
+    const int cols = (int)((n + 255) / 256) * nl;
+    int nchunks = std::max(1, std::min((B + 7) / 8, (148 * 8 + cols - 1) / cols));
+    nchunks = (int)std::min<long>(nchunks, cap);
+    const int chunk = (B + nchunks - 1) / nchunks;
+    nchunks = (B + chunk - 1) / chunk;
+    u64* F = E;
+    u64* part = F + 6 * ls;
+    cudaMemsetAsync(F, 0, 2 * ls * sizeof(u64), st);
+    cudaMemcpyAsync(F + 2 * ls, acc, 2 * ls * sizeof(u64), cudaMemcpyDeviceToDevice, st);
+    cudaMemsetAsync(F + 4 * ls, 0, 2 * ls * sizeof(u64), st);
+    rot_partial_kernel<<<dim3((n + 255) / 256, nl, nchunks), 256, 0, st>>>(d, B, l, chunk, ct, gal, ACC, T, part);
+    accum_fold_kernel<<<dim3((n + 255) / 256, 6 * nl), 256, 0, st>>>(d, nl, nchunks, part, F);
+    note_launch(2);
+    launch_ntt<true>(d, JobRotAcc{F, acc, l, d}, 2 * nl, st);
+    return true;
+}
+
 // Hoisted rotations (P3 of SURVEY.md): decompose + ModUp the source once; per
 // step only the automorphism-gathered inner product and ModDown remain.
 void rotate_hoisted(const Dev& d, int R, int l, const u64* src, const u32* gal,

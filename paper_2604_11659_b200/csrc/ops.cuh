@@ -54,6 +54,10 @@ void mult_relin_rescale_batch(const Dev& d, int B, int l, ItemPtr a, ItemPtr b, 
 // Rotation of B cts at level l by Galois elements gal[b] with keys[b].
 void rotate_batch(const Dev& d, int B, int l, ItemPtr ct, const u32* gal, const u64* const* keys,
                   ItemPtr out, u64* scratch, cudaStream_t st);
+// Rotate B items and add them into acc [2][l+1][n] (one ModDown NTT per
+// output limb); false (nothing launched) when the scratch is too small.
+bool rotate_accumulate(const Dev& d, int B, int l, ItemPtr ct, const u32* gal, const u64* const* keys,
+                       u64* acc, u64* scratch, cudaStream_t st);
 // Hoisted rotations of ONE source ct into R outputs (one per step).
 void rotate_hoisted(const Dev& d, int R, int l, const u64* src, const u32* gal,
                     const u64* const* keys, ItemPtr out, u64* scratch, cudaStream_t st);

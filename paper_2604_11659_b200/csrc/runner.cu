@@ -501,11 +501,14 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, cons
         rescale_batch(d, bn, L - 1, 2, strided(Mb, (size_t)2 * L * n), strided(Cb, ctL2),
                       ItemPtr{nullptr, nullptr, 0}, Tb, st);
         // accumulation rotations (step-0 pairs form the sorted prefix)
-        if (bn - z > 0)
+        accumulate(d, z, L - 1, 2, strided(Cb, ctL2), out, st);
+        static const bool split_rot = getenv("HS_SPLIT_ROTATE_ACCUM") != nullptr;
+        if (bn - z > 0 && (split_rot || !rotate_accumulate(d, bn - z, L - 2, strided(Cb + (size_t)z * ctL2, ctL2),
+                                                           dG + s + z, dK + s + z, out, ks, st))) {
             rotate_batch(d, bn - z, L - 2, strided(Cb + (size_t)z * ctL2, ctL2), dG + s + z, dK + s + z,
                          strided(Fb + (size_t)z * ctL2, ctL2), ks, st);
-        accumulate(d, z, L - 1, 2, strided(Cb, ctL2), out, st);
-        accumulate(d, bn - z, L - 1, 2, strided(Fb + (size_t)z * ctL2, ctL2), out, st);
+            accumulate(d, bn - z, L - 1, 2, strided(Fb + (size_t)z * ctL2, ctL2), out, st);
+        }
         KP.release(bsteps);
     }
     cudaError_t e = cudaGetLastError();
