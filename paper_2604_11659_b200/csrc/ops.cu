@@ -612,6 +612,40 @@ struct JobModDownRescale {                   // forward NTT, job = (b*2+c)*l+m, 
     }
 };
 
+// u = INTT(out_l) of the relinearised ct's top limb without forming out_l:
+// out_l = (acc_l - NTT_l(lift_p T)) p^-1 + add_l, so by linearity
+//   INTT(out_l) = INTT(acc_l p^-1 + add_l) - lift_l(T) p^-1      (mod q_l)
+// -- one inverse NTT instead of a forward NTT followed by an inverse one.
+template <class Add>
+struct JobTopU {                             // inverse NTT, job = b*2+c, prime l
+    const u64* T;
+    const u64* ACC;
+    u64* U;                                  // [bc][n]
+    Add add;
+    int l;
+    Dev d;
+    struct Ctx {
+        const u64 *t, *acc;
+        u64* u;
+        typename Add::B add;
+        ulonglong2 w;        // p^-1 mod q_l
+    };
+    HS_DEV Ctx make(int bc) const {
+        return Ctx{T + (size_t)bc * d.n, ACC + ((size_t)bc * (l + 2) + l) * d.n, U + (size_t)bc * d.n,
+                   add.bind(bc >> 1, bc & 1, l, l, d), d.auxinv[l]};
+    }
+    HS_DEV int prime(const Ctx&) const { return l; }
+    HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst& P) const {
+        return shoup_lazy(__ldg(c.acc + j), c.w.x, c.w.y, P.q) + add.v(c.add, j, d, P);   // [0, 3q)
+    }
+    HS_DEV u64* scratch(const Ctx& c) const { return c.u; }
+    HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst& P) const {
+        const u64 y = shoup(v, P.n_inv, P.n_inv_sh, P.q);
+        const u64 t = shoup(lift_mod(__ldg(c.t + j), d.aux_q, P), c.w.x, c.w.y, P.q);
+        c.u[j] = sub_mod(y, t, P.q);
+    }
+};
+
 void mult_relin_rescale_batch(const Dev& d, int B, int l, ItemPtr a, ItemPtr b, const u64* const* keys,
                               ItemPtr mask_mont, ItemPtr top, ItemPtr out, u64* scratch, u64* U,
                               cudaStream_t st) {
@@ -625,9 +659,14 @@ void mult_relin_rescale_batch(const Dev& d, int B, int l, ItemPtr a, ItemPtr b, 
     modup_and_inner(d, B, l, D, E, keys, ACC, st);
     launch_ntt<false>(d, JobInvGather{strided(ACC, (size_t)(l + 2) * n), 1, l + 2, l + 1, d.L + 1, T, n},
                       B * 2, st);
-    // limb l of the relinearised ct (into top, ct layout [2][l+1][n]), then its INTT
-    launch_ntt<true>(d, JobModDown<AddTensor>{T, ACC, top, add, l, d, l, 1}, B * 2, st);
-    launch_ntt<false>(d, JobInvGather{top, 2, l + 1, l, l, U, n}, B * 2, st);
+    // u = INTT of limb l of the relinearised ct
+    static const bool top_fwd = getenv("HS_TOPLIMB_FWD") != nullptr;   // A/B: old two-transform path
+    if (top_fwd) {
+        launch_ntt<true>(d, JobModDown<AddTensor>{T, ACC, top, add, l, d, l, 1}, B * 2, st);
+        launch_ntt<false>(d, JobInvGather{top, 2, l + 1, l, l, U, n}, B * 2, st);
+    } else {
+        launch_ntt<false>(d, JobTopU<AddTensor>{T, ACC, U, add, l, d}, B * 2, st);
+    }
     launch_ntt<true>(d,
                      JobModDownRescale<AddTensor>{T, U, ACC, out, mask_mont, add, l, d,
                                                   d.qlinv + (size_t)l * (d.L + 1)},
