@@ -268,54 +268,64 @@ constexpr int KSI_T = 256;
 #endif
 constexpr int kKsiUnroll = KSI_UNROLL;
 
+#ifndef KSI_IPB
+#define KSI_IPB 4                    // A/B cfg2: 1 -> 126.3 ms, 2 -> 125.0, 4 -> 124.7
+#endif
+constexpr int kKsiIpb = KSI_IPB;             // items per CTA (loads of the next item overlap)
+
 __global__ void __launch_bounds__(KSI_T, 4)
-ks_inner_kernel(Dev d, int l, const u64* __restrict__ E, size_t e_item_stride,
+ks_inner_kernel(Dev d, int l, int B, const u64* __restrict__ E, size_t e_item_stride,
                 const u64* const* __restrict__ keys, const u32* __restrict__ gal,
                 u64* __restrict__ ACC) {
     const u32 n = d.n;
     const u32 k = 2 * (blockIdx.x * KSI_T + threadIdx.x);
     const int m = blockIdx.y;
-    const int b = blockIdx.z;
     if (k >= n) return;
     const int pm = m <= l ? m : d.L + 1;
-    const u32 g = gal ? gal[b] : 0u;
-    const u32 src0 = g ? galois_perm(k, g, d.log_n) : k;
-    const u32 src1 = g ? galois_perm(k + 1, g, d.log_n) : k + 1;
-    const u64* __restrict__ Ei = E + (size_t)b * e_item_stride + (size_t)m * n;
-    const size_t estride = (size_t)(l + 2) * n;                    // one digit of E
-    const u64* key = keys[b];
-    const size_t kstride = (size_t)(d.L + 2) * n;                  // one digit of a key
-    const ulonglong2* __restrict__ kb = (const ulonglong2*)(key + (size_t)pm * n + k);
-    const ulonglong2* __restrict__ ka =
-        (const ulonglong2*)(key + (size_t)(d.L + 1) * kstride + (size_t)pm * n + k);
-    const size_t kst2 = kstride / 2;
-    u64 lb0 = 0, hb0 = 0, la0 = 0, ha0 = 0, lb1 = 0, hb1 = 0, la1 = 0, ha1 = 0;
-#pragma unroll kKsiUnroll
-    for (int i = 0; i <= l; i++, Ei += estride, kb += kst2, ka += kst2) {
-        u64 e0, e1;
-        if (g) {
-            e0 = __ldg(Ei + src0);
-            e1 = __ldg(Ei + src1);
-        } else {
-            const ulonglong2 ee = __ldg((const ulonglong2*)(Ei + k));
-            e0 = ee.x;
-            e1 = ee.y;
-        }
-        const ulonglong2 vb = __ldg(kb), va = __ldg(ka);
-        mac128(lb0, hb0, e0, vb.x);
-        mac128(lb1, hb1, e1, vb.y);
-        mac128(la0, ha0, e0, va.x);
-        mac128(la1, ha1, e1, va.y);
-    }
     const PrimeConst P = d.pc[pm];
-    u64* out = ACC + (size_t)b * 2 * (l + 2) * n;
-    *(ulonglong2*)(out + (size_t)m * n + k) = make_ulonglong2(reduce128(lb0, hb0, P), reduce128(lb1, hb1, P));
-    *(ulonglong2*)(out + ((size_t)(l + 2) + m) * n + k) =
-        make_ulonglong2(reduce128(la0, ha0, P), reduce128(la1, ha1, P));
+    const size_t estride = (size_t)(l + 2) * n;                    // one digit of E
+    const size_t kstride = (size_t)(d.L + 2) * n;                  // one digit of a key
+    const size_t kst2 = kstride / 2;
+#pragma unroll
+    for (int bb = 0; bb < kKsiIpb; bb++) {
+        const int b = blockIdx.z * kKsiIpb + bb;
+        if (b >= B) break;
+        const u32 g = gal ? gal[b] : 0u;
+        const u32 src0 = g ? galois_perm(k, g, d.log_n) : k;
+        const u32 src1 = g ? galois_perm(k + 1, g, d.log_n) : k + 1;
+        const u64* __restrict__ Ei = E + (size_t)b * e_item_stride + (size_t)m * n;
+        const u64* key = keys[b];
+        const ulonglong2* __restrict__ kb = (const ulonglong2*)(key + (size_t)pm * n + k);
+        const ulonglong2* __restrict__ ka =
+            (const ulonglong2*)(key + (size_t)(d.L + 1) * kstride + (size_t)pm * n + k);
+        u64 lb0 = 0, hb0 = 0, la0 = 0, ha0 = 0, lb1 = 0, hb1 = 0, la1 = 0, ha1 = 0;
+#pragma unroll kKsiUnroll
+        for (int i = 0; i <= l; i++, Ei += estride, kb += kst2, ka += kst2) {
+            u64 e0, e1;
+            if (g) {
+                e0 = __ldg(Ei + src0);
+                e1 = __ldg(Ei + src1);
+            } else {
+                const ulonglong2 ee = __ldg((const ulonglong2*)(Ei + k));
+                e0 = ee.x;
+                e1 = ee.y;
+            }
+            const ulonglong2 vb = __ldg(kb), va = __ldg(ka);
+            mac128(lb0, hb0, e0, vb.x);
+            mac128(lb1, hb1, e1, vb.y);
+            mac128(la0, ha0, e0, va.x);
+            mac128(la1, ha1, e1, va.y);
+        }
+        u64* out = ACC + (size_t)b * 2 * (l + 2) * n;
+        *(ulonglong2*)(out + (size_t)m * n + k) =
+            make_ulonglong2(reduce128(lb0, hb0, P), reduce128(lb1, hb1, P));
+        *(ulonglong2*)(out + ((size_t)(l + 2) + m) * n + k) =
+            make_ulonglong2(reduce128(la0, ha0, P), reduce128(la1, ha1, P));
+    }
 }
 
 static dim3 ks_inner_grid(const Dev& d, int l, int B) {
-    return dim3((d.n + 2 * KSI_T - 1) / (2 * KSI_T), l + 2, B);
+    return dim3((d.n + 2 * KSI_T - 1) / (2 * KSI_T), l + 2, (B + kKsiIpb - 1) / kKsiIpb);
 }
 
 // ModDown addends (what is added to the key-switch output), bound per CTA.
@@ -518,7 +528,7 @@ static void modup_and_inner(const Dev& d, int B, int l, u64* D, u64* E, const u6
     static const bool fused = getenv("HS_MODUP_FUSED") != nullptr;
     if (!fused) {
         launch_ntt<true>(d, JobModUp{D, E, l, d.L, d.n, d.pc}, B * (l + 1) * (l + 1), st);
-        ks_inner_kernel<<<ks_inner_grid(d, l, B), KSI_T, 0, st>>>(d, l, E, (size_t)(l + 1) * (l + 2) * d.n,
+        ks_inner_kernel<<<ks_inner_grid(d, l, B), KSI_T, 0, st>>>(d, l, B, E, (size_t)(l + 1) * (l + 2) * d.n,
                                                                  keys, nullptr, ACC);
         note_launch();
         return;
@@ -534,7 +544,7 @@ static void modup_and_inner(const Dev& d, int B, int l, u64* D, u64* E, const u6
     }
     // small rings: whole-limb single-pass NTT, then the plain inner product
     launch_ntt<true>(d, JobModUp{D, E, l, d.L, d.n, d.pc}, B * (l + 1) * (l + 1), st);
-    ks_inner_kernel<<<ks_inner_grid(d, l, B), KSI_T, 0, st>>>(d, l, E, (size_t)(l + 1) * (l + 2) * d.n, keys,
+    ks_inner_kernel<<<ks_inner_grid(d, l, B), KSI_T, 0, st>>>(d, l, B, E, (size_t)(l + 1) * (l + 2) * d.n, keys,
                                                              nullptr, ACC);
     note_launch();
 }
@@ -793,7 +803,7 @@ void rotate_hoisted(const Dev& d, int R, int l, const u64* src, const u32* gal,
     ItemPtr s = strided(src, 0);
     launch_ntt<false>(d, JobDecompose<SrcPlain>{SrcPlain{s, 1}, E, D, d.df, l, n, d}, l + 1, st);
     launch_ntt<true>(d, JobModUp{D, E, l, d.L, n, d.pc}, (l + 1) * (l + 1), st);
-    ks_inner_kernel<<<ks_inner_grid(d, l, R), KSI_T, 0, st>>>(d, l, E, 0, keys, gal, ACC);
+    ks_inner_kernel<<<ks_inner_grid(d, l, R), KSI_T, 0, st>>>(d, l, R, E, 0, keys, gal, ACC);
     note_launch();
     mod_down(d, R, l, ACC, T, AddPermC0{s, gal}, out, st);
 }
