@@ -208,6 +208,12 @@ def cpu_oracle_sample(wl, sample_pairs: int, nthreads: int):
     ca = ctx.encrypt(ctx.encode(va), keys)
     cb = ctx.encrypt(ctx.encode(vb), keys)
     pairs = O.pair_schedule_csr_csc(oa, ia, ob, ib, dim)[:sample_pairs]
+    # host-memory bound: the oracle holds its Galois keys in RAM (681 MB each
+    # at N=2^16, L=24), so shrink the sample until its keys fit ~16 GB
+    key_bytes = 2 * (P.levels + 1) * (P.levels + 2) * P.ring_degree * 8
+    max_keys = max(1, int(16e9 // key_bytes))
+    while len(pairs) > 1 and len(O.rotation_steps(pairs, dim)) > max_keys:
+        pairs = pairs[:max(1, len(pairs) // 2)]
     ctx.gen_galois_keys(O.rotation_steps(pairs, dim), keys)
     L = P.levels
     masks = {p: ctx.encode(np.eye(1, dim * dim, p).ravel(), scale=float(P.modulus_chain[L - 1]),

@@ -317,6 +317,12 @@ constexpr int kIoUnroll = NTT_IO_UNROLL;   // (#pragma arguments are not macro-e
 #define NTT_STAGED_FIRST 0
 #endif
 
+// Shared-memory exchange buffers per CTA: 2 = double-buffered (one barrier
+// per exchange), 1 = single buffer (an extra barrier before each reuse).
+#ifndef NTT_NBUF
+#define NTT_NBUF 1             // A/B cfg2|cfg3s: 2 -> 125.0|892 ms, 1 -> 123.0|856, 1 + 8 CTAs/SM -> 120.5|850
+#endif
+
 // LOGN (log2 ring degree) and S0 (first stage of the pass) are template
 // parameters so every index shift/mask below is a compile-time constant.
 template <bool FWD, bool FIRST, bool LAST, int LOGG, int H, int C, int EPT, int LOGN, int S0, class Job>
@@ -413,7 +419,8 @@ struct PassEngine {
         if constexpr (I < NR) {
             constexpr int rp = FWD ? I - 1 : NR - I;        // previous round
             constexpr int r = FWD ? I : NR - 1 - I;
-            u64* buf = sm + (I & 1) * SMW;
+            u64* buf = sm + (NTT_NBUF == 2 ? (I & 1) * SMW : 0);
+            if constexpr (NTT_NBUF == 1) __syncthreads();   // previous readers of the buffer
             scatter<rp>(buf, v, E);
             __syncthreads();
             gather<r>(buf, v, E);
@@ -459,7 +466,8 @@ struct PassEngine {
                 for (int e = 0; e < ML::NU; e++) out(job, E, j0 + e * gstride, v[k * ML::NU + e]);
             }
         } else {
-            u64* buf = sm + (NR & 1) * SMW;   // the buffer not written by the last exchange
+            u64* buf = sm + (NTT_NBUF == 2 ? (NR & 1) * SMW : 0);   // not written by the last exchange
+            if constexpr (NTT_NBUF == 1) __syncthreads();
             scatter<RLAST>(buf, v, E);
             __syncthreads();
 #pragma unroll kIoUnroll
@@ -472,7 +480,7 @@ struct PassEngine {
 };
 
 #ifndef NTT_MINB
-#define NTT_MINB 6            // CTAs/SM for 16 elements per thread (128 threads)
+#define NTT_MINB 8            // CTAs/SM for 16 elements per thread (128 threads; 64 registers)
 #endif
 #ifndef NTT_MINB8
 #define NTT_MINB8 4           // for 8 elements per thread (256 threads)
@@ -481,7 +489,7 @@ template <bool FWD, bool FIRST, bool LAST, int LOGG, int H, int C, int EPT, int 
 __global__ void __launch_bounds__(((H << LOGG) * C) / EPT, EPT >= 16 ? NTT_MINB : NTT_MINB8)
 ntt_pass_kernel(Dev d, Job job, int jbase) {
     using PE = PassEngine<FWD, FIRST, LAST, LOGG, H, C, EPT, LOGN, S0, Job>;
-    __shared__ u64 sm[2 * PE::SMW];
+    __shared__ u64 sm[NTT_NBUF * PE::SMW];
     typename PE::Env E;
     const int jb = jbase + (int)blockIdx.y;
     E.jc = job.make(jb);

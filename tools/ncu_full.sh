@@ -6,7 +6,7 @@
 set -u
 TAG=${1:-r01}
 WL=${2:-cfg2}
-KEEP=${3:-modup_inner}
+KEEP=${3:-^$}
 OUT=gpurun_out
 cap() {  # name regex skip count
   local rep="$OUT/${TAG}_$1"
@@ -21,9 +21,9 @@ cap() {  # name regex skip count
     if ! echo "$1" | grep -Eq "$KEEP"; then rm -f "$rep.ncu-rep"; fi
   fi
 }
-cap modup_inner 'modup_inner' 0 1
-cap moddown_tensor 'AddTensor' 0 2
-cap rescale 'JobRescale' 0 2
-cap modup_passA 'JobModUp' 4 1
+cap ks_inner 'ks_inner' 2 1
+cap moddown_rescale 'JobModDownRescale' 0 2
+cap modup 'JobModUp' 2 2
+cap topu 'JobTopU' 0 2
 cap invgather 'JobInvGather' 0 2
-cap decompose 'SrcTensor' 0 2
+cap rot_partial 'rot_partial' 0 1
