@@ -303,7 +303,7 @@ HS_DEV void unit_butterflies(u64* v, const ulonglong2* __restrict__ tw, u32 Y, u
 // loops: these inline the job's loader/epilogue, so full unrolling of 16
 // copies of a heavy epilogue costs instruction-cache misses.
 #ifndef NTT_IO_UNROLL
-#define NTT_IO_UNROLL 4            // A/B at cfg2: 16 -> 174.0 ms, 4 -> 167.5, 2 -> 171.0
+#define NTT_IO_UNROLL 8            // A/B at cfg2: 16 -> 174.0 ms, 4 -> 167.5, 2 -> 171.0 (6 CTAs/SM); at 8 CTAs/SM: 2 -> 121.4, 4 -> 121.0, 8 -> 120.0
 #endif
 constexpr int kIoUnroll = NTT_IO_UNROLL;   // (#pragma arguments are not macro-expanded)
 // 1: rounds with two units per thread run them as a rolled loop (one copy of

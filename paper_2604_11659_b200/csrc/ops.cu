@@ -273,7 +273,10 @@ constexpr int kKsiUnroll = KSI_UNROLL;
 #endif
 constexpr int kKsiIpb = KSI_IPB;             // items per CTA (loads of the next item overlap)
 
-__global__ void __launch_bounds__(KSI_T, 4)
+#ifndef KSI_MINB
+#define KSI_MINB 4                   // A/B cfg2: 4 -> 121 ms, 5 -> 125, 6 -> 133
+#endif
+__global__ void __launch_bounds__(KSI_T, KSI_MINB)
 ks_inner_kernel(Dev d, int l, int B, const u64* __restrict__ E, size_t e_item_stride,
                 const u64* const* __restrict__ keys, const u32* __restrict__ gal,
                 u64* __restrict__ ACC) {
