@@ -227,6 +227,12 @@ class CkksContext:
             if r in keys.galois or r in extra or r in todo:
                 continue
             todo.append(r)
+        if device and todo and min(int(q) for q in (*self.params.modulus_chain,
+                                                    self.params.aux_prime)) <= 0xFFFFFFFF:
+            # numpy's integers(0, q) takes its buffered 32-bit Lemire path
+            # when q - 1 fits 32 bits; keygen.cu replays the 64-bit path only,
+            # so such chains draw on the host (bit-identical, just slower)
+            device = False
         if device and todo:
             from .rng import galois_states
             self._ensure_device_keygen(keys)
@@ -419,8 +425,29 @@ class CkksContext:
         if keys.galois.get(r) is None:
             raise KeyMissingError(f"missing Galois key for step {steps}")
         out = D.empty((2, ct.level + 1, self._n))
-        check(lib().hs_eval_rotate(self._h, D.ptr(ct.data), D.ptr(out), ct.level, r, D.stream()))
+        made = self._materialise_lazy([r])
+        try:
+            check(lib().hs_eval_rotate(self._h, D.ptr(ct.data), D.ptr(out), ct.level, r, D.stream()))
+        finally:
+            self._drop_materialised(made)
         return Ciphertext(out, ct.scale, ct.level)
+
+    def _materialise_lazy(self, steps) -> list:
+        """Generate lazily registered Galois keys (gen_galois_keys(device=
+        "lazy")) that a single eval_rotate needs; returns the steps made."""
+        lazy = getattr(self, "_lazy_steps", ())
+        todo = sorted({r for r in steps if r in lazy and not lib().hs_key_has(self._h, 1, r)})
+        if todo:
+            from .rng import galois_states
+            st = np.ascontiguousarray(galois_states(self.params.seed, todo))
+            check(lib().hs_key_generate_galois(self._h, (ctypes.c_uint32 * len(todo))(*todo),
+                                               st.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                                               len(todo), D.stream()))
+        return todo
+
+    def _drop_materialised(self, steps) -> None:
+        for r in steps:
+            check(lib().hs_key_drop(self._h, 1, r))
 
     def eval_rotate_hoisted(self, ct: Ciphertext, steps, keys: KeyBundle) -> list:
         """Several rotations of one ciphertext sharing one decomposition/ModUp
@@ -441,8 +468,12 @@ class CkksContext:
         if todo:
             ptrs = (ctypes.c_void_p * len(todo))(*[o.data_ptr() for _, o in todo])
             st = (ctypes.c_uint32 * len(todo))(*[r for r, _ in todo])
-            check(lib().hs_eval_rotate_hoisted(self._h, D.ptr(ct.data), ptrs, st, len(todo),
-                                               ct.level, D.stream()))
+            made = self._materialise_lazy([r for r, _ in todo])
+            try:
+                check(lib().hs_eval_rotate_hoisted(self._h, D.ptr(ct.data), ptrs, st, len(todo),
+                                                   ct.level, D.stream()))
+            finally:
+                self._drop_materialised(made)
         return outs
 
 

@@ -18,8 +18,8 @@
 
 namespace hs {
 
-constexpr int CRT_MAXW = 40;       // 64-bit words of Q (<= 40 * 64 bits)
-constexpr int CRT_MAXL = 40;       // limbs
+constexpr int CRT_MAXW = 64;       // 64-bit words of Q (63 limbs of < 61 bits fit 60 words)
+constexpr int CRT_MAXL = 64;       // limbs (hs_ctx_create accepts L <= 62: 63 limbs)
 
 struct CrtArgs {
     const u64* coeff;              // [nl][n] coefficient domain, canonical

@@ -6,7 +6,7 @@ So each rank runs a contiguous share of the step-sorted pair list
 (hs_spmspm_* with shard=(rank, world)) against its full key replica and
 produces a partial result ciphertext; the only exchange is one integer SUM
 of those partials followed by a mod-q kernel.  world * q < 2^63 (P6), so an
-int64 SUM is exact; NCCL over NVLink moves 2(L-1) limbs per rank.
+int64 SUM is exact (as uint64 bits; checked: world * max q < 2^64); NCCL over NVLink moves 2(L-1) limbs per rank.
 """
 
 from __future__ import annotations
@@ -18,6 +18,7 @@ import torch.distributed as dist
 from . import device as D
 from ._lib import check, lib
 from .encmat import EncryptedResult
+from .errors import ParameterError
 from .engine import MaskCache, OpCounter, run_pairs
 from .types import Ciphertext
 
@@ -48,6 +49,11 @@ def spmm_csr_csc_distributed(enc_a, enc_b, ctx, keys, counter: OpCounter | None 
     counter = counter if counter is not None else OpCounter()
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
+    qmax = max(int(q) for q in ctx.params.modulus_chain)
+    if world * qmax >= 1 << 64:
+        # the int64 SUM of canonical partials is exact only while world*q < 2^64
+        raise ParameterError(f"{world} ranks x {qmax.bit_length()}-bit moduli overflow the "
+                             "64-bit partial sum")
     res = run_pairs(enc_a, enc_b, ctx, keys, counter, mask_cache, None, shard=(rank, world))
     if res.ctxt is None:
         return res

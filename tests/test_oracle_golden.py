@@ -75,10 +75,49 @@ def _ops_pipeline(O, key):
     return P, ctx, keys, ct_a, ct_b
 
 
+@pytest.fixture(scope="module")
+def golden_big():
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                           "golden_big.json")) as fh:
+        return json.load(fh)
+
+
 @pytest.mark.parametrize("key", ["64_40_2_7", "64_40_3_7", "1024_45_2_2024", "16384_50_2_2024"])
 def test_ckks_primitives_match_reference(golden, oracle_mod, key):
+    _check_primitives(oracle_mod, golden["ops"][key], key)
+
+
+# the north-star parameters (N = 2^16, L = 24: a 25-digit x 26-modulus key
+# switch) and a chain with scaling primes < 2^32 (numpy's 32-bit Lemire path);
+# (2^17, L = 35) is checked on the GPU only (its six keys take 17 GB of RAM)
+@pytest.mark.parametrize("key", ["1024_30_2_2024", "65536_50_24_2024"])
+def test_ckks_primitives_match_reference_big(golden_big, oracle_mod, key):
+    _check_primitives(oracle_mod, golden_big["ops"][key], key)
+
+
+def test_limb_kernels_match_reference_L24(golden_big, oracle_mod):
     O = oracle_mod
-    rec = golden["ops"][key]
+    key = "65536_50_24_2024"
+    n, sb, L, seed = parse_key(key)
+    ctx = O.OracleContext(O.build_params(n, sb, L, seed))
+    for pi_s, rec in golden_big["kernels"][key].items():
+        pi = int(pi_s)
+        q = rec["q"]
+        t = ctx.tables(pi)
+        a, b, acc, s = kernel_inputs(q, n, pi)
+        dg = rec["digests"]
+        assert digest(O.ntt(a, q, t["roots"], t["roots_sh"])) == dg["ntt"], pi
+        assert digest(O.intt(a, q, t["iroots"], t["iroots_sh"], t["n_inv"])) == dg["intt"], pi
+        assert digest(O.mul_mod(a, b, q, t["mu"])) == dg["mul"], pi
+        assert digest(O.extend_mod(a, q, rec["q_dst"])) == dg["extend"], pi
+        f = acc.copy()
+        O.fma_mod(f, a, b, q, t["mu"])
+        assert digest(f) == dg["fma"], pi
+
+
+def _check_primitives(O, rec, key):
     P, ctx, keys, (ca, sa, la), (cb, sbb, lb) = _ops_pipeline(O, key)
     L = P.levels
     slots = P.slots
@@ -141,8 +180,17 @@ def oracle_runner_case(O, n, sb, L, seed, dim, sparsity, mseed):
 
 
 def test_runner_matches_reference(golden, oracle_mod):
-    O = oracle_mod
-    for key, rec in golden["runner"].items():
+    _check_runner_cases(oracle_mod, golden["runner"])
+
+
+def test_runner_matches_reference_big(golden_big, oracle_mod):
+    """4x4 @50% at N = 2^16, L = 24 (16 pairs, 15 Galois keys) and 8x8 @50%
+    with scaling primes < 2^32."""
+    _check_runner_cases(oracle_mod, golden_big["runner"])
+
+
+def _check_runner_cases(O, cases):
+    for key, rec in cases.items():
         n, sb, L, seed = rec["params"]
         P, ctx, keys, a, b, ca, cb, pairs, res = oracle_runner_case(
             O, n, sb, L, seed, rec["dim"], rec["sparsity"], rec["mseed"])
