@@ -2,23 +2,36 @@
 """Benchmark: encrypted SpMSpM (CKKS, CSR/C) on B200 -- BASELINE.json metric.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--workload cfg3|cfg2|...]
 
 A "step" is one full encrypted SpMSpM (the reference's timed region:
-planning + every pair, engine.py:176-184) of the workload below.  Inputs
-(the two encrypted matrices, keys, masks) are resident in HBM for ``value``;
-``e2e`` repeats the step through the public API with host-resident
-ciphertexts (host->device copy of both operands and device->host copy of the
-result inside the timed region).
+planning + every pair, engine.py:176-184) of the workload below, run through
+the public API (engine.spmm_csr_csc) once per step.  Each step's timed region
+starts from PINNED HOST ciphertexts: the host->device copy of both operands,
+the matmul, and the device->host copy of the result ciphertext.  ``e2e`` is
+that wall time; ``value`` is the same execution's device time between CUDA
+events recorded after the inputs are resident in HBM and before the result
+copy (so both numbers come from one execution per step).
 
-Workload (BASELINE.json configs[1], the largest single-GPU config whose keys
-fit one B200): ring degree 2^14, Delta = 2^50, L = 2, 64x64 @ 75% sparsity,
-matrices from the reference harness seeds (bench.py:93-96 of the reference:
-cell seed 1*1_000_003 + 64*1_009), params seed 2024.
+Workload (default: BASELINE.json configs[2], the config the metric is quoted
+on): ring degree 2^16, Delta = 2^50, L = 24, 128x128 @ 90% sparsity, CSR/C
+with hoisted alignment rotations; the 12,956 Galois keys (8.8 TB) cannot be
+stored, so they are generated on the device inside every step, bit-exact
+with the reference's numpy streams.  Matrices from the reference harness
+seeds (bench.py:93-96 of the reference: cell seed 1*1_000_003 + 128*1_009),
+params seed 2024.  ``--workload cfg2`` = configs[1] (2^14, L = 2, 64x64 @75%).
 
 Metric: ct-ops/s = logical OpCounter total (ct_ct_mults + pt_mults +
 rotations + relins + rescales + adds; relin no-ops excluded) / seconds, and
 ms per matmul.  Multi-GPU (torchrun, one rank per GPU): pairs are sharded
-(strong scaling: fixed matmul), partial results combined by one NCCL SUM.
+(strong scaling: fixed matmul), partial results combined by one NCCL SUM;
+times are the max over ranks.
+
+Roofline: the key-switch kernels are timed inside the timed steps with CUDA
+events on their own launching stream (hs_probe_*): the ModUp NTT passes and
+the key inner product; the one with the larger share of the step is the
+``roofline`` entry (HBM GB/s vs MEASURED_PEAKS.json), with its INT-pipe
+fraction against the butterfly peak measured on this GPU (hs_int_peak).
 
 ``--impl reference`` times the reference algorithm on the host CPU instead:
 the CPU oracle (oracle/, a C restatement of the reference path, bit-exact,
@@ -48,11 +61,11 @@ WORKLOADS = {
     # configs[2]: N=2^16, L=24; 12,956 Galois keys (8.8 TB) are generated on
     # the device on demand inside the timed step (they cannot be stored).
     "cfg3": dict(ring_degree=1 << 16, scale_bits=50, levels=24, seed=2024, dim=128, sparsity=0.9,
-                 lazy_keys=True, batch_gb=16,
+                 lazy_keys=True, batch_gb=16, cpu_sample_pairs=16,
                  desc="configs[2]: N=2^16, L=24, 128x128 @90%, hoisted rotations, "
                       "Galois keys generated on device inside the step"),
     "cfg3s": dict(ring_degree=1 << 16, scale_bits=50, levels=24, seed=2024, dim=32, sparsity=0.9,
-                  lazy_keys=True, batch_gb=16,
+                  lazy_keys=True, batch_gb=16, cpu_sample_pairs=16,
                   desc="N=2^16, L=24, 32x32 @90% (cfg3 parameters, smaller matrix)"),
     # configs[3] scale: 256x256 needs 65,536 slots > 32,768 at N=2^16 -> 2x2 tiles of 128x128
     # (tiling.py; beyond the reference's one-ciphertext capacity)
@@ -191,92 +204,162 @@ def logical_ct_ops(pairs: np.ndarray, dim: int) -> int:
 
 # ------------------------------------------------------------ CPU baseline
 
-def cpu_oracle_sample(wl, sample_pairs: int, nthreads: int):
-    """Time the CPU oracle (reference algorithm restated in C, bit-exact) on
-    the first ``sample_pairs`` pairs of the workload.  Returns (seconds,
-    ct_ops, pairs_used).  Keys for the sampled steps only."""
-    from oracle import oracle as O
-    P = O.build_params(wl["ring_degree"], wl["scale_bits"], wl["levels"], wl["seed"])
-    ctx = O.OracleContext(P)
-    keys = ctx.keygen()
-    dim = wl["dim"]
-    seed = cell_seed(dim)
-    a = O.generate_random_sparse(dim, wl["sparsity"], (seed, 0))
-    b = O.generate_random_sparse(dim, wl["sparsity"], (seed, 1))
-    oa, ia, va = O.csr_pack(a)
-    ob, ib, vb = O.csc_pack(b)
-    ca = ctx.encrypt(ctx.encode(va), keys)
-    cb = ctx.encrypt(ctx.encode(vb), keys)
-    pairs = O.pair_schedule_csr_csc(oa, ia, ob, ib, dim)[:sample_pairs]
-    # host-memory bound: the oracle holds its Galois keys in RAM (681 MB each
-    # at N=2^16, L=24), so shrink the sample until its keys fit ~16 GB
-    key_bytes = 2 * (P.levels + 1) * (P.levels + 2) * P.ring_degree * 8
-    max_keys = max(1, int(16e9 // key_bytes))
-    while len(pairs) > 1 and len(O.rotation_steps(pairs, dim)) > max_keys:
-        pairs = pairs[:max(1, len(pairs) // 2)]
-    ctx.gen_galois_keys(O.rotation_steps(pairs, dim), keys)
-    L = P.levels
-    masks = {p: ctx.encode(np.eye(1, dim * dim, p).ravel(), scale=float(P.modulus_chain[L - 1]),
-                           level=L - 1)[0] for p in {min(x[2], x[3]) for x in pairs}}
-    t0 = time.perf_counter()
-    ctx.spmspm(ca[0], cb[0], pairs, dim, masks, keys, nthreads=nthreads)
-    dt = time.perf_counter() - t0
-    return dt, logical_ct_ops(np.array(pairs, dtype=np.int64).reshape(-1, 4), dim), len(pairs)
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+class OracleSample:
+    """The CPU oracle (the reference algorithm restated in C, bit-exact,
+    OpenMP over pairs) on a bounded sample of the workload's pairs.
+
+    Setup (keygen, encryption, Galois keys and masks of the sampled pairs --
+    outside the reference's timed region too, hespmm/bench.py:130-152) runs
+    once; ``run()`` times one pass over the sample.  The sample takes pairs in
+    schedule order while their Galois keys fit the host-memory budget (the
+    oracle keeps keys in RAM: 681 MB each at N=2^16, L=24), at least one pair
+    per host thread so every thread is busy, and ``max_pairs`` at most.
+    """
+
+    def __init__(self, wl, max_pairs: int, nthreads: int):
+        from oracle import oracle as O
+        self.O = O
+        P = O.build_params(wl["ring_degree"], wl["scale_bits"], wl["levels"], wl["seed"])
+        self.ctx = ctx = O.OracleContext(P)
+        self.keys = keys = ctx.keygen()
+        dim = self.dim = wl["dim"]
+        seed = cell_seed(dim)
+        a = O.generate_random_sparse(dim, wl["sparsity"], (seed, 0))
+        b = O.generate_random_sparse(dim, wl["sparsity"], (seed, 1))
+        oa, ia, va = O.csr_pack(a)
+        ob, ib, vb = O.csc_pack(b)
+        self.ca = ctx.encrypt(ctx.encode(va), keys)
+        self.cb = ctx.encrypt(ctx.encode(vb), keys)
+        allp = O.pair_schedule_csr_csc(oa, ia, ob, ib, dim)
+        self.total_pairs = len(allp)
+        key_bytes = 2 * (P.levels + 1) * (P.levels + 2) * P.ring_degree * 8
+        try:
+            import psutil
+            avail = psutil.virtual_memory().available
+        except ImportError:
+            avail = 32e9
+        max_keys = max(2, int(min(0.4 * avail, 48e9) // key_bytes))
+        want = max(nthreads, min(max_pairs, len(allp)))
+        pairs, steps = [], set()
+        for p in allp:
+            s_p = set(O.rotation_steps([p], dim))
+            if len(steps | s_p) > max_keys:
+                continue
+            steps |= s_p
+            pairs.append(p)
+            if len(pairs) >= want:
+                break
+        self.pairs = pairs
+        self.threads = min(nthreads, len(pairs))
+        ctx.gen_galois_keys(sorted(steps), keys)
+        L = P.levels
+        self.masks = {q: ctx.encode(np.eye(1, dim * dim, q).ravel(), scale=float(P.modulus_chain[L - 1]),
+                                    level=L - 1)[0] for q in {min(x[2], x[3]) for x in pairs}}
+        self.ct_ops = logical_ct_ops(np.array(pairs, dtype=np.int64).reshape(-1, 4), dim)
+
+    def run(self) -> float:
+        t0 = time.perf_counter()
+        self.ctx.spmspm(self.ca[0], self.cb[0], self.pairs, self.dim, self.masks, self.keys,
+                        nthreads=self.threads)
+        return time.perf_counter() - t0
+
+    def describe(self) -> str:
+        return (f"{len(self.pairs)} of {self.total_pairs} pairs per step (schedule order, keys "
+                f"within host RAM), oracle/hs_oracle.c, OpenMP {self.threads} threads")
 
 
 # ------------------------------------------------------------- roofline
 
-def roofline_traffic(workload: str):
-    """DRAM bytes per probe launch from the committed ncu capture of the same
-    probe (tools/roofline_probe.py -> profiles/r01_roofline_traffic.json)."""
+def roofline_traffic(workload: str, kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture of
+    the same workload (profiles/r02_roofline_traffic.json)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_roofline_traffic.json")) as fh:
-            return json.load(fh).get(workload)
+        with open(os.path.join(ROOT, "profiles", "r02_roofline_traffic.json")) as fh:
+            return json.load(fh).get(workload, {}).get(kernel)
     except (OSError, ValueError):
         return None
 
 
-def roofline_probe(pkg, ctx, params, peaks, reps=10, workload=None):
-    """Time the dominant kernel alone with CUDA events on its launch stream.
+PROBE_MODUP, PROBE_KS_INNER = 1, 2
+PROBE_NAMES = {PROBE_MODUP: "ntt_pass_kernel<JobModUp> (ModUp NTT passes of the key switch)",
+               PROBE_KS_INNER: "ks_inner_kernel (key inner product)"}
 
-    Dominant kernel: the NTT pass kernel (ntt_pass_kernel), which carries
-    decomposition, ModUp, ModDown and rescale (see profiles/).  Probe: one
-    batched forward NTT over the ModUp limb count of a pair batch; one launch
-    = one pass over every limb; algorithmic bytes per launch = limbs * 16 n
-    (each limb read once, written once).
-    """
-    import torch
+
+def probe_read(kind: int) -> dict:
+    import ctypes
+    from paper_2604_11659_b200._lib import check, lib
+    out = (ctypes.c_double * 4)()
+    check(lib().hs_probe_read(kind, out))
+    return {"launches": out[0], "ms": out[1], "bytes": out[2], "work": out[3]}
+
+
+def int_peak(q: int) -> dict:
+    import ctypes
     from paper_2604_11659_b200 import device as D
     from paper_2604_11659_b200._lib import check, lib
-    n, L = params.ring_degree, params.levels
-    # ModUp limb count of a pair batch, capped at ~2 GiB of limbs
-    items = max(1, min(512, (2 << 30) // (8 * n * (L + 1) * (L + 2))))
-    limbs = items * (L + 1) * (L + 2)
-    buf = D.zeros((limbs, n))
-    st = torch.cuda.current_stream()
-    for _ in range(3 if reps > 1 else 0):
-        check(lib().hs_ntt(ctx.handle, D.ptr(buf), items * (L + 1), L + 2, 0, 0, D.stream()))
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    e0.record(st)
-    for _ in range(reps):
-        check(lib().hs_ntt(ctx.handle, D.ptr(buf), items * (L + 1), L + 2, 0, 0, D.stream()))
-    e1.record(st)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / (reps * 2)           # two pass launches per NTT
-    algo = limbs * 16 * n
-    achieved = algo / (ms * 1e-3) / 1e9
+    out = (ctypes.c_double * 4)()
+    check(lib().hs_int_peak(int(q), out, D.stream()))
+    return {"butterflies_per_s": out[0], "imad_per_s": out[1], "iadd_per_s": out[2], "sms": int(out[3])}
+
+
+def roofline_entry(kind: int, rec: dict, peaks: dict, ipk: dict | None, workload: str,
+                   step_ms_total: float) -> dict:
     peak = peaks.get("hbm_gbs", 6650.0)
-    butterflies = limbs * (n // 2) * (n.bit_length() - 1) / 2      # per pass
-    tr = roofline_traffic(workload) if workload else None
-    return {"kernel": "ntt_pass_kernel (batched 2-pass NTT, one pass)", "bound": "hbm",
-            "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4),
-            "traffic": tr["dram_bytes_per_launch"] if tr else None,
-            "traffic_source": tr["source"] if tr else None,
-            "launch_ms": round(ms, 4), "algorithmic_bytes_per_launch": algo,
-            "butterflies_per_launch": int(butterflies),
-            "peak_source": "MEASURED_PEAKS.json" if "hbm_gbs" in peaks else "fallback"}
+    launches = max(rec["launches"], 1.0)
+    launch_ms = rec["ms"] / launches
+    achieved = rec["bytes"] / (rec["ms"] * 1e-3) / 1e9 if rec["ms"] else 0.0
+    tr = roofline_traffic(workload, "modup" if kind == PROBE_MODUP else "ks_inner")
+    e = {"kernel": PROBE_NAMES[kind], "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+         "unit": "GB/s", "frac": round(achieved / peak, 4),
+         "traffic": tr["dram_bytes_per_launch"] if tr else None,
+         "traffic_source": tr["source"] if tr else None,
+         "launches_timed": int(rec["launches"]), "launch_ms": round(launch_ms, 4),
+         "algorithmic_bytes_per_launch": int(rec["bytes"] / launches),
+         "share_of_step": round(rec["ms"] / step_ms_total, 4),
+         "timing": "CUDA events on the launching stream around every launch inside the timed steps",
+         "peak_source": "MEASURED_PEAKS.json" if "hbm_gbs" in peaks else "fallback 6650 GB/s"}
+    if kind == PROBE_MODUP and ipk:
+        bps = rec["work"] / (rec["ms"] * 1e-3) if rec["ms"] else 0.0
+        e["int_pipe"] = {"achieved": round(bps / 1e9, 2), "peak": round(ipk["butterflies_per_s"] / 1e9, 2),
+                         "unit": "G butterflies/s", "frac": round(bps / ipk["butterflies_per_s"], 4),
+                         "peak_source": "hs_int_peak: the engine's forward butterfly on "
+                                        "register-resident data, measured on this GPU"}
+    elif kind == PROBE_KS_INNER:
+        e["int_pipe"] = {"achieved": round(rec["work"] / (rec["ms"] * 1e-3) / 1e9, 2) if rec["ms"] else 0.0,
+                         "unit": "G 64x64->128-bit MACs/s"}
+    return e
+
+
+def ks_hbm_floor(params, pairs: np.ndarray, dim: int, peak_gbs: float) -> dict:
+    """BASELINE.md section 3 key-switch HBM floor of one step:
+    bytes_KS(l, B) = 16n(l+1)(l+2)/B + 24n(l+1) per key switch, with each
+    distinct key read once (B = the key switches sharing it)."""
+    n, L = params.ring_degree, params.levels
+    key = lambda l: 16 * n * (l + 1) * (l + 2)
+    ct = lambda l: 24 * n * (l + 1)
+    P = len(pairs)
+    mn = np.minimum(pairs[:, 2], pairs[:, 3])
+    al = np.abs(pairs[:, 2] - pairs[:, 3])
+    src = np.where(pairs[:, 2] > pairs[:, 3], 0, 1)
+    align = {(int(o), int(s)) for o, s in zip(src[al > 0], al[al > 0])}
+    acc_steps = mn - (pairs[:, 0] * dim + pairs[:, 1])
+    acc = acc_steps[acc_steps != 0]
+    slots = n // 2
+    keys_align = {s % slots for _, s in align}
+    keys_acc = {int(s) % slots for s in acc}
+    b = key(L) + P * ct(L)                                    # relinearisation (one key)
+    b += len(keys_align) * key(L) + len(align) * ct(L)         # hoisted alignment rotations
+    b += len(keys_acc) * key(L - 2) + len(acc) * ct(L - 2)     # accumulation rotations
+    return {"bytes": int(b), "floor_ms": round(b / (peak_gbs * 1e9) * 1e3, 2),
+            "key_switches": int(P + len(align) + len(acc)),
+            "distinct_keys": int(len(keys_align | keys_acc) + 1)}
 
 
 def load_peaks():
@@ -297,15 +380,15 @@ def run_reference_arm(args, wl):
         print(json.dumps({"impl": "reference", "unavailable": "the reference packs one matrix per "
                           "ciphertext and raises CapacityError beyond its slots (no tiling)"}))
         return
-    nthreads = os.cpu_count() or 1
+    nthreads = host_threads()
+    t0 = time.time()
+    samp = OracleSample(wl, args.cpu_sample_pairs, nthreads)
+    log(f"[bench] reference arm setup {time.time() - t0:.1f}s: {samp.describe()}")
     for _ in range(args.warmup):
-        pass                                    # the CPU oracle has no warm-up state
-    times, ops = [], 0
-    for _ in range(args.steps):
-        dt, ops, used = cpu_oracle_sample(wl, args.cpu_sample_pairs, nthreads)
-        times.append(dt)
+        samp.run()
+    times = [samp.run() for _ in range(args.steps)]
     sec = float(np.mean(times))
-    value = ops / sec
+    value = samp.ct_ops / sec
     line = {
         "impl": "reference", "metric": "encrypted SpMSpM ct-ops/s (CSR/C)", "value": value,
         "unit": "ct-ops/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -313,10 +396,10 @@ def run_reference_arm(args, wl):
         "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": {"workload": wl["desc"], "ring_degree": wl["ring_degree"],
                    "levels": wl["levels"], "scale_bits": wl["scale_bits"], "dim": wl["dim"],
-                   "sparsity": wl["sparsity"], "sample_pairs": used},
-        "cpu_baseline": {"value": value, "unit": "ct-ops/s", "cores": nthreads, "kind": "port",
-                         "sample": f"first {used} pairs of the CSR/C schedule per step "
-                                   "(oracle/hs_oracle.c, OpenMP over pairs)"},
+                   "sparsity": wl["sparsity"], "sample_pairs": len(samp.pairs),
+                   "pairs": samp.total_pairs},
+        "cpu_baseline": {"value": value, "unit": "ct-ops/s", "cores": samp.threads, "kind": "port",
+                         "sample": samp.describe()},
         "e2e": {"value": value, "unit": "ct-ops/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -334,10 +417,9 @@ def run_b200_arm(args, wl):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2604_11659_b200 as pkg
-    from paper_2604_11659_b200 import device as D
     from paper_2604_11659_b200 import dist as hdist
     from paper_2604_11659_b200 import encmat, engine
-    from paper_2604_11659_b200._lib import lib
+    from paper_2604_11659_b200._lib import check, lib
     from paper_2604_11659_b200.types import Ciphertext
 
     params, ctx, keys, a, b, ea, eb, pairs, mc = make_inputs(pkg, wl)
@@ -365,82 +447,93 @@ def run_b200_arm(args, wl):
         return torch.from_numpy(e.ctxt.host()).pin_memory()
 
     def operand_from_host(e, h):
+        """The operand rebuilt on pinned host limbs, then uploaded by the API
+        (Ciphertext.data: host -> HBM copy)."""
         if tiled:
-            return tiling.TiledMatrix(e.n, e.T, e.b, e.layout, {
+            m = tiling.TiledMatrix(e.n, e.T, e.b, e.layout, {
                 k: encmat.EncryptedSparseMatrix(Ciphertext(h[k], t.ctxt.scale, t.ctxt.level), t.meta)
                 for k, t in e.tiles.items()})
-        return encmat.EncryptedSparseMatrix(Ciphertext(h, e.ctxt.scale, e.ctxt.level), e.meta)
+            for t in m.tiles.values():
+                t.ctxt.data
+            return m
+        m = encmat.EncryptedSparseMatrix(Ciphertext(h, e.ctxt.scale, e.ctxt.level), e.meta)
+        m.ctxt.data
+        return m
 
     def host_bytes(h):
         return sum(x.numel() * 8 for x in h.values()) if tiled else h.numel() * 8
 
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
-    res, c = step(ea, eb)
-    assert c.ct_ops() == ct_ops
-    for _ in range(max(0, args.warmup - 1)):
-        step(ea, eb)
-    torch.cuda.synchronize()
-
-    # ---- device-resident timed region
-    st = torch.cuda.current_stream()
-    launches0 = lib().hs_launch_count()
-    total_ms = 0.0
-    with ClockSampler(local) as clk:
-        for _ in range(args.steps):
-            flush.fill_(1)
-            if world > 1:
-                dist.barrier()
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(st)
-            res, c = step(ea, eb)
-            e1.record(st)
-            torch.cuda.synchronize()
-            total_ms += e0.elapsed_time(e1)
-    launches = lib().hs_launch_count() - launches0
-    if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    ms = total_ms / args.steps
-    value = ct_ops / (ms * 1e-3)
-
-    # ---- end to end through the public API from pinned host buffers
     host_a = operand_host(ea)
     host_b = operand_host(eb)
-    e2e_s = 0.0
-    d2h = 0
-    for _ in range(args.steps):
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+    st = torch.cuda.current_stream()
+
+    def one_step():
+        """One execution: H2D of both operands (from pinned host limbs), the
+        matmul through the public API, D2H of the result ciphertext."""
         flush.fill_(1)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0 = time.perf_counter()
         ha = operand_from_host(ea, host_a)
         hb = operand_from_host(eb, host_b)
-        r, _ = step(ha, hb)
-        out = result_host(r)
-        e2e_s += time.perf_counter() - t0
-        d2h = out.nbytes
-    if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e_value = ct_ops / (e2e_s / args.steps)
+        e0.record(st)
+        res, c = step(ha, hb)
+        e1.record(st)
+        out = result_host(res)
+        t1 = time.perf_counter()
+        torch.cuda.synchronize()
+        return out, c, e0.elapsed_time(e1), (t1 - t0) * 1e3
 
-    # ---- bit-exactness spot check of the timed result (cheap: vs the first run)
-    same = bool(np.array_equal(result_host(res), out))
+    first, c, _, _ = one_step()
+    assert c.ct_ops() == ct_ops, (c.ct_ops(), ct_ops)
+    for _ in range(max(0, args.warmup - 1)):
+        one_step()
+
+    # ---- timed region: K executions; kernel probes armed inside it
+    check(lib().hs_probe_arm((1 << PROBE_MODUP) | (1 << PROBE_KS_INNER)))
+    launches0 = lib().hs_launch_count()
+    dev_ms, e2e_ms, same = 0.0, 0.0, True
+    d2h = 0
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            out, c, dms, wms = one_step()
+            dev_ms += dms
+            e2e_ms += wms
+            d2h = out.nbytes
+            same &= bool(np.array_equal(out, first))
+    launches = lib().hs_launch_count() - launches0
+    probes = {k: probe_read(k) for k in (PROBE_MODUP, PROBE_KS_INNER)}
+    check(lib().hs_probe_arm(0))
+    if world > 1:
+        t = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms, e2e_ms = float(t[0]), float(t[1])
+    ms = dev_ms / args.steps
+    value = ct_ops / (ms * 1e-3)
+    e2e_value = ct_ops / (e2e_ms / args.steps * 1e-3)
 
     peaks = load_peaks()
-    roof = roofline_probe(pkg, ctx, params, peaks, workload=args.workload) if rank == 0 else None
+    roof = other = ipk = None
+    ks_floor = None
+    if rank == 0:
+        ipk = int_peak(params.modulus_chain[1])
+        ents = {k: roofline_entry(k, probes[k], peaks, ipk, args.workload, dev_ms) for k in probes}
+        top = max(ents, key=lambda k: probes[k]["ms"])
+        roof = ents[top]
+        other = ents[PROBE_KS_INNER if top == PROBE_MODUP else PROBE_MODUP]
+        if not tiled:
+            ks_floor = ks_hbm_floor(params, pairs, dim, peaks.get("hbm_gbs", 6650.0))
+            ks_floor["frac_of_step"] = round(ks_floor["floor_ms"] / ms, 4)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not tiled:
-        nthreads = os.cpu_count() or 1
-        dt, ops_s, used = cpu_oracle_sample(wl, args.cpu_sample_pairs, nthreads)
-        cpu = {"value": ops_s / dt, "unit": "ct-ops/s", "cores": nthreads, "kind": "port",
-               "sample": f"first {used} of {len(pairs)} pairs (oracle/hs_oracle.c, OpenMP), "
-                         f"{dt:.1f}s"}
+        samp = OracleSample(wl, args.cpu_sample_pairs, host_threads())
+        dt = samp.run()
+        cpu = {"value": samp.ct_ops / dt, "unit": "ct-ops/s", "cores": samp.threads, "kind": "port",
+               "sample": samp.describe() + f", {dt:.1f}s"}
     if world > 1:
         dist.barrier()
     if rank == 0:
@@ -453,12 +546,17 @@ def run_b200_arm(args, wl):
                        "levels": wl["levels"], "scale_bits": wl["scale_bits"], "dim": wl["dim"],
                        "sparsity": wl["sparsity"], "pairs": int(len(pairs)), "ct_ops": ct_ops,
                        "galois_keys": len(keys.galois), "parallelism": f"pair-shard x{world}",
-                       "l2": "flushed between steps (256 MiB write)"},
+                       "l2": "flushed between steps (256 MiB write)",
+                       "timing": "one execution per step: value = CUDA events around the matmul "
+                                 "(inputs resident), e2e = wall time incl. H2D + D2H"},
             "e2e": {"value": e2e_value, "unit": "ct-ops/s",
                     "h2d_bytes_per_step": int(host_bytes(host_a) + host_bytes(host_b)),
-                    "d2h_bytes_per_step": int(d2h), "ms_per_matmul": e2e_s / args.steps * 1e3},
+                    "d2h_bytes_per_step": int(d2h), "ms_per_matmul": e2e_ms / args.steps},
             "gpu_launches": int(launches),
             "roofline": roof,
+            "roofline_other": other,
+            "ks_hbm_floor": ks_floor,
+            "int_peak": ipk,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "result_repeatable": same,
@@ -474,11 +572,14 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
-    ap.add_argument("--cpu-sample-pairs", type=int, default=1024)
+    ap.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS))
+    ap.add_argument("--cpu-sample-pairs", type=int, default=0,
+                    help="CPU sample size (pairs); 0 = the workload's default")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
+    if not args.cpu_sample_pairs:
+        args.cpu_sample_pairs = wl.get("cpu_sample_pairs", 1024)
     if args.impl == "reference":
         run_reference_arm(args, wl)
     else:

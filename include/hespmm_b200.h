@@ -59,6 +59,20 @@ const char* hs_version(void);
 /* Total kernels launched by this library since load (benchmark evidence). */
 int64_t hs_launch_count(void);
 
+/* Measurement hooks for bench.py's roofline line (no reference counterpart).
+ * hs_probe_arm(mask): every later launch of an armed kernel class (bit k of
+ * mask arms kind k: 1 = the ModUp NTT passes of the key switch, 2 = the key
+ * inner product; 0 = off) records a CUDA event pair on its own launching
+ * stream; arming clears the record.  hs_probe_read(kind, out4) synchronises
+ * on those events and returns {launches, total ms, algorithmic DRAM bytes,
+ * integer work (butterflies resp. 64x64-bit MACs)} of that kind.
+ * hs_int_peak(q, out4, stream): integer-pipe peaks measured on this GPU:
+ * {NTT butterflies/s (the engine's butterfly, register-resident, prime q),
+ *  mad.wide.u32/s, 32-bit add instructions/s, SMs}. */
+hs_status hs_probe_arm(int32_t mask);
+hs_status hs_probe_read(int32_t kind, double* out4);
+hs_status hs_int_peak(uint64_t q, double* out4, void* stream);
+
 /* ---------------------------------------------------------------- context
  * Replaces CkksContext.__init__ precomputation (ckks/context.py:31-58) and
  * PrimeTables (ckks/params.py:87-112): NTT twiddles (psi = first g in

@@ -35,6 +35,9 @@ _SIGS = {
     "hs_last_error": (ctypes.c_char_p, []),
     "hs_version": (ctypes.c_char_p, []),
     "hs_launch_count": (ctypes.c_int64, []),
+    "hs_probe_arm": (ctypes.c_int, [ctypes.c_int32]),
+    "hs_probe_read": (ctypes.c_int, [ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]),
+    "hs_int_peak": (ctypes.c_int, [ctypes.c_uint64, ctypes.POINTER(ctypes.c_double), c_vp]),
     "hs_ctx_create": (ctypes.c_int, [ctypes.POINTER(c_vp), ctypes.c_int, ctypes.c_uint32,
                                      ctypes.c_uint32, c_u64p, ctypes.c_uint64]),
     "hs_ctx_destroy": (None, [c_vp]),

@@ -15,12 +15,65 @@
 
 #include <atomic>
 #include <cstdlib>
+#include <vector>
 
 namespace hs {
 
 static std::atomic<long long> g_launches{0};
 void note_launch(int count) { g_launches += count; }
 long long launch_count() { return g_launches.load(); }
+
+// ---- in-step kernel timer
+namespace {
+struct ProbeRec {
+    cudaEvent_t e0, e1;
+    int kind, launches;
+    double bytes, work;
+};
+std::vector<ProbeRec> g_probe;       // event pool; [0, g_probe_used) recorded since the last read
+size_t g_probe_used = 0;
+int g_probe_kind = 0;                // bit k arms kind k
+}  // namespace
+
+ProbeScope::ProbeScope(int kind, cudaStream_t s, double bytes, double work, int launches) : st(s) {
+    if (kind == PROBE_NONE || !((g_probe_kind >> kind) & 1)) return;
+    if (g_probe_used == g_probe.size()) {
+        ProbeRec r{};
+        if (cudaEventCreate(&r.e0) != cudaSuccess || cudaEventCreate(&r.e1) != cudaSuccess) return;
+        g_probe.push_back(r);
+    }
+    slot = (int)g_probe_used++;
+    ProbeRec& r = g_probe[slot];
+    r.kind = kind;
+    r.launches = launches;
+    r.bytes = bytes;
+    r.work = work;
+    cudaEventRecord(r.e0, st);
+}
+ProbeScope::~ProbeScope() {
+    if (slot >= 0) cudaEventRecord(g_probe[slot].e1, st);
+}
+void probe_arm(int mask) {
+    g_probe_kind = mask;
+    g_probe_used = 0;
+}
+// {launches, total ms, algorithmic bytes, integer work} of the launches of
+// `kind` recorded since the last arm (arming again clears the record).
+int probe_read(int kind, double* out4) {
+    out4[0] = out4[1] = out4[2] = out4[3] = 0.0;
+    for (size_t k = 0; k < g_probe_used; k++) {
+        ProbeRec& r = g_probe[k];
+        if (r.kind != kind) continue;
+        if (cudaEventSynchronize(r.e1) != cudaSuccess) return 1;
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, r.e0, r.e1) != cudaSuccess) return 1;
+        out4[0] += r.launches;
+        out4[1] += ms;
+        out4[2] += r.bytes;
+        out4[3] += r.work;
+    }
+    return 0;
+}
 
 // =========================================================== helpers
 
@@ -522,17 +575,34 @@ static void launch_modup_inner(const Dev& d, int B, int l, u64* D, u64* E, const
 }
 
 // ModUp + inner product for B items (E must hold x_i df_i in slot (i, i)).
+// Algorithmic DRAM bytes of one ks_inner launch: E read once, each of the
+// nkeys distinct keys read once (repeat uses hit L2), ACC written once.
+static double ks_inner_bytes(const Dev& d, int l, int B, int nkeys) {
+    const double limb = 8.0 * d.n, ml = (double)(l + 1) * (l + 2);
+    return B * ml * limb + nkeys * 2.0 * ml * limb + B * 2.0 * (l + 2) * limb;
+}
+
 static void modup_and_inner(const Dev& d, int B, int l, u64* D, u64* E, const u64* const* keys,
-                            u64* ACC, cudaStream_t st) {
+                            u64* ACC, cudaStream_t st, int nkeys) {
     // Default: ModUp as a batched two-pass NTT writing E, then the streaming
     // inner-product kernel (both run at high occupancy).  HS_MODUP_FUSED=1
     // selects the fused pass-B + inner-product kernel (no E round trip, but
     // 128-bit accumulators cap it at 25% occupancy).
     static const bool fused = getenv("HS_MODUP_FUSED") != nullptr;
     if (!fused) {
-        launch_ntt<true>(d, JobModUp{D, E, l, d.L, d.n, d.pc}, B * (l + 1) * (l + 1), st);
-        ks_inner_kernel<<<ks_inner_grid(d, l, B), KSI_T, 0, st>>>(d, l, B, E, (size_t)(l + 1) * (l + 2) * d.n,
-                                                                 keys, nullptr, ACC);
+        const double jobs = (double)B * (l + 1) * (l + 1), n = d.n;
+        {
+            // algorithmic bytes: each pass reads and writes one limb per job
+            ProbeScope ps(PROBE_MODUP, st, jobs * 32.0 * n, jobs * (n / 2) * d.log_n, 2);
+            launch_ntt<true>(d, JobModUp{D, E, l, d.L, d.n, d.pc}, B * (l + 1) * (l + 1), st);
+        }
+        {
+            ProbeScope ps(PROBE_KS_INNER, st, ks_inner_bytes(d, l, B, nkeys),
+                          (double)B * 2 * (l + 1) * (l + 2) * n);
+            ks_inner_kernel<<<ks_inner_grid(d, l, B), KSI_T, 0, st>>>(d, l, B, E,
+                                                                     (size_t)(l + 1) * (l + 2) * d.n,
+                                                                     keys, nullptr, ACC);
+        }
         note_launch();
         return;
     }
@@ -554,25 +624,26 @@ static void modup_and_inner(const Dev& d, int B, int l, u64* D, u64* E, const u6
 
 template <class Src, class Add>
 static void key_switch_batch(const Dev& d, int B, int l, const Src& src, const Add& add,
-                             const u64* const* keys, ItemPtr out, u64* scratch, cudaStream_t st) {
+                             const u64* const* keys, ItemPtr out, u64* scratch, cudaStream_t st,
+                             int nkeys) {
     const u32 n = d.n;
     u64* E = scratch;
     u64* D = E + (size_t)B * (l + 1) * (l + 2) * n;
     u64* ACC = D + (size_t)B * (l + 1) * n;
     u64* T = ACC + (size_t)B * 2 * (l + 2) * n;
     launch_ntt<false>(d, JobDecompose<Src>{src, E, D, d.df, l, n, d}, B * (l + 1), st);
-    modup_and_inner(d, B, l, D, E, keys, ACC, st);
+    modup_and_inner(d, B, l, D, E, keys, ACC, st, nkeys);
     mod_down(d, B, l, ACC, T, add, out, st);
 }
 
 void relin_batch(const Dev& d, int B, int l, ItemPtr ct3, const u64* const* keys, ItemPtr out,
                  u64* scratch, cudaStream_t st) {
-    key_switch_batch(d, B, l, SrcPlain{ct3, 2}, AddPoly{ct3}, keys, out, scratch, st);
+    key_switch_batch(d, B, l, SrcPlain{ct3, 2}, AddPoly{ct3}, keys, out, scratch, st, 1);
 }
 
 void mult_relin_batch(const Dev& d, int B, int l, ItemPtr a, ItemPtr b, const u64* const* keys,
                       ItemPtr out, u64* scratch, cudaStream_t st) {
-    key_switch_batch(d, B, l, SrcTensor{a, b}, AddTensor{a, b}, keys, out, scratch, st);
+    key_switch_batch(d, B, l, SrcTensor{a, b}, AddTensor{a, b}, keys, out, scratch, st, 1);
 }
 
 // ModDown followed by rescale, merged.  Both subtract the NTT of a lifted
@@ -669,7 +740,7 @@ void mult_relin_rescale_batch(const Dev& d, int B, int l, ItemPtr a, ItemPtr b, 
     u64* T = ACC + (size_t)B * 2 * (l + 2) * n;
     const AddTensor add{a, b};
     launch_ntt<false>(d, JobDecompose<SrcTensor>{SrcTensor{a, b}, E, D, d.df, l, n, d}, B * (l + 1), st);
-    modup_and_inner(d, B, l, D, E, keys, ACC, st);
+    modup_and_inner(d, B, l, D, E, keys, ACC, st, 1);       // the relin key, shared
     launch_ntt<false>(d, JobInvGather{strided(ACC, (size_t)(l + 2) * n), 1, l + 2, l + 1, d.L + 1, T, n},
                       B * 2, st);
     // u = INTT of limb l of the relinearised ct
@@ -688,7 +759,7 @@ void mult_relin_rescale_batch(const Dev& d, int B, int l, ItemPtr a, ItemPtr b, 
 
 void rotate_batch(const Dev& d, int B, int l, ItemPtr ct, const u32* gal, const u64* const* keys,
                   ItemPtr out, u64* scratch, cudaStream_t st) {
-    key_switch_batch(d, B, l, SrcPerm{ct, gal}, AddPermC0{ct, gal}, keys, out, scratch, st);
+    key_switch_batch(d, B, l, SrcPerm{ct, gal}, AddPermC0{ct, gal}, keys, out, scratch, st, B);
 }
 
 // Rotate B items and add them all into acc ([2][l+1][n]), with ONE ModDown
@@ -761,7 +832,7 @@ struct JobRotAcc {                           // forward NTT, job = c*(l+1)+m
 __global__ void accum_fold_kernel(Dev d, int nl, int nchunks, const u64* part, u64* acc);
 
 bool rotate_accumulate(const Dev& d, int B, int l, ItemPtr ct, const u32* gal, const u64* const* keys,
-                       u64* acc, u64* scratch, cudaStream_t st) {
+                       u64* acc, u64* scratch, cudaStream_t st, int nkeys) {
     const u32 n = d.n;
     const int nl = l + 1;
     const size_t ls = (size_t)nl * n;
@@ -774,7 +845,7 @@ bool rotate_accumulate(const Dev& d, int B, int l, ItemPtr ct, const u32* gal, c
     u64* ACC = D + (size_t)B * (l + 1) * n;
     u64* T = ACC + (size_t)B * 2 * (l + 2) * n;
     launch_ntt<false>(d, JobDecompose<SrcPerm>{SrcPerm{ct, gal}, E, D, d.df, l, n, d}, B * (l + 1), st);
-    modup_and_inner(d, B, l, D, E, keys, ACC, st);
+    modup_and_inner(d, B, l, D, E, keys, ACC, st, nkeys);
     launch_ntt<false>(d, JobInvGather{strided(ACC, (size_t)(l + 2) * n), 1, l + 2, l + 1, d.L + 1, T, n},
                       B * 2, st);
     const int cols = (int)((n + 255) / 256) * nl;

@@ -24,6 +24,19 @@ inline ItemPtr table(const u64* const* tab) { return ItemPtr{tab, nullptr, 0}; }
 
 PrimeConst make_prime_const(u64 q, u32 n);
 long long launch_count();
+
+// In-step kernel timer (bench.py's roofline line).  hs_probe_arm(kind) arms
+// one kernel class; every launch of that class then records a CUDA event
+// pair on its own launching stream around it, with the launch's algorithmic
+// DRAM bytes and integer work (butterflies or 64x64 MACs).  hs_probe_read
+// synchronises and returns {launches, total ms, bytes, work}.
+enum ProbeKind { PROBE_NONE = 0, PROBE_MODUP = 1, PROBE_KS_INNER = 2, PROBE_KINDS = 3 };
+struct ProbeScope {
+    int slot = -1;
+    cudaStream_t st;
+    ProbeScope(int kind, cudaStream_t st, double bytes, double work, int launches = 1);
+    ~ProbeScope();
+};
 inline PrimeMap prime_map_range(int first, int count) {
     PrimeMap m{};
     m.nl = count;
@@ -57,7 +70,7 @@ void rotate_batch(const Dev& d, int B, int l, ItemPtr ct, const u32* gal, const 
 // Rotate B items and add them into acc [2][l+1][n] (one ModDown NTT per
 // output limb); false (nothing launched) when the scratch is too small.
 bool rotate_accumulate(const Dev& d, int B, int l, ItemPtr ct, const u32* gal, const u64* const* keys,
-                       u64* acc, u64* scratch, cudaStream_t st);
+                       u64* acc, u64* scratch, cudaStream_t st, int nkeys);
 // Hoisted rotations of ONE source ct into R outputs (one per step).
 void rotate_hoisted(const Dev& d, int R, int l, const u64* src, const u32* gal,
                     const u64* const* keys, ItemPtr out, u64* scratch, cudaStream_t st);

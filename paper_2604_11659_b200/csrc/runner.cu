@@ -504,7 +504,8 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, cons
         accumulate(d, z, L - 1, 2, strided(Cb, ctL2), out, st);
         static const bool split_rot = getenv("HS_SPLIT_ROTATE_ACCUM") != nullptr;
         if (bn - z > 0 && (split_rot || !rotate_accumulate(d, bn - z, L - 2, strided(Cb + (size_t)z * ctL2, ctL2),
-                                                           dG + s + z, dK + s + z, out, ks, st))) {
+                                                           dG + s + z, dK + s + z, out, ks, st,
+                                                           (int)bsteps.size()))) {
             rotate_batch(d, bn - z, L - 2, strided(Cb + (size_t)z * ctL2, ctL2), dG + s + z, dK + s + z,
                          strided(Fb + (size_t)z * ctL2, ctL2), ks, st);
             accumulate(d, bn - z, L - 1, 2, strided(Fb + (size_t)z * ctL2, ctL2), out, st);

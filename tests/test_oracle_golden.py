@@ -207,3 +207,16 @@ def _check_runner_cases(O, cases):
         out = dec.reshape(rec["dim"], rec["dim"])
         assert repr(O.frobenius_error(out, O.plain_matmul(a, b))) == rec["frobenius"], key
         assert digest(out.view(np.uint64)) == rec["decoded"], key
+
+
+@pytest.mark.parametrize("key", ["64_35_2_3", "1024_45_2_2024", "16384_50_2_2024"])
+def test_product_prime_tables_match_reference(golden, key):
+    """paper_2604_11659_b200.params.prime_tables (the reference's table API,
+    ckks/params.py:87-112) against the reference's own table digests."""
+    from paper_2604_11659_b200.params import prime_tables
+    n = parse_key(key)[0]
+    for pi_s, rec in golden["kernels"][key].items():
+        t = prime_tables(rec["q"], n)
+        assert t.mu == rec["mu"] and t.n_inv == rec["n_inv"]
+        for name in ("roots", "roots_sh", "iroots", "iroots_sh"):
+            assert digest(getattr(t, name)) == rec["digests"][name], (key, pi_s, name)
