@@ -384,6 +384,167 @@ static dim3 ks_inner_grid(const Dev& d, int l, int B) {
     return dim3((d.n + 2 * KSI_T - 1) / (2 * KSI_T), l + 2, (B + kKsiIpb - 1) / kKsiIpb);
 }
 
+// ---- the key inner product with bulk-async (TMA engine) row streaming.
+//
+// Same sums as ks_inner_kernel for the un-permuted case (every pair-batch key
+// switch): ACC[b][c][m][k] = sum_i E[b][i][m][k] * K_b[c][i][m][k].  One CTA
+// owns a 256-coefficient column tile of one target modulus m for KSI2_IPB
+// consecutive items.  A producer warp streams the rows of each (item, digit)
+// -- E (2 KB), key b-half (2 KB), key a-half (2 KB) -- into a KSI2_NST-stage
+// shared-memory ring with cp.async.bulk (no registers, no address math in the
+// consumers), completion signalled on per-stage mbarriers; 4 consumer warps
+// (2 coefficients per thread) wait on a stage, multiply-accumulate in 128
+// bits, and release it on an "empty" mbarrier.  Grid x = item group (fastest),
+// so the CTAs sharing a key tile (the relinearisation key: every item) run
+// back to back and the key rows come from L2 after the first read
+// (E is streamed with an evict-first hint, keys with evict-last).
+constexpr int KSI2_CT = 128;                 // consumer threads
+constexpr int KSI2_C = 2 * KSI2_CT;          // coefficients per tile
+constexpr int KSI2_ROWB = KSI2_C * 8;        // bytes per row tile
+#ifndef KSI2_NST
+#define KSI2_NST 6
+#endif
+#ifndef KSI2_IPB
+#define KSI2_IPB 2
+#endif
+constexpr int kKsi2Nst = KSI2_NST, kKsi2Ipb = KSI2_IPB;
+constexpr size_t KSI2_SMEM = (size_t)kKsi2Nst * 3 * KSI2_ROWB;
+
+HS_DEV u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+HS_DEV void mbar_init(u32 bar, u32 count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+HS_DEV void mbar_wait(u32 bar, u32 parity) {
+    u32 ok;
+    do {
+        asm volatile("{\n\t.reg .pred p;\n\t"
+                     "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(ok)
+                     : "r"(bar), "r"(parity)
+                     : "memory");
+    } while (!ok);
+}
+HS_DEV void mbar_arrive(u32 bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+HS_DEV void mbar_expect_tx(u32 bar, u32 bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+HS_DEV void bulk_g2s(u32 dst, const void* src, u32 bytes, u32 bar, u64 policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(policy)
+        : "memory");
+}
+
+__global__ void __launch_bounds__(KSI2_CT + 32)
+ks_inner_tma_kernel(Dev d, int l, int B, const u64* __restrict__ E, size_t e_item_stride,
+                    const u64* const* __restrict__ keys, u64* __restrict__ ACC) {
+    extern __shared__ __align__(128) unsigned char ksi2_smem[];
+    __shared__ __align__(8) unsigned long long bars[2 * kKsi2Nst];     // full, empty
+    const u32 n = d.n;
+    const int m = blockIdx.z;
+    const u32 col0 = blockIdx.y * KSI2_C;
+    const int b0 = blockIdx.x * kKsi2Ipb;
+    const int nb = min(kKsi2Ipb, B - b0);
+    const int pm = m <= l ? m : d.L + 1;
+    const u32 tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const u32 smb = smem_u32(ksi2_smem);
+    const u32 full0 = smem_u32(&bars[0]), empty0 = smem_u32(&bars[kKsi2Nst]);
+    if (tid == 0) {
+        for (int s = 0; s < kKsi2Nst; s++) {
+            mbar_init(full0 + 8 * s, 1);
+            mbar_init(empty0 + 8 * s, KSI2_CT / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == KSI2_CT / 32) {                                     // producer warp
+        if (lane == 0) {
+            u64 pol_e, pol_k;
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_e));
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_k));
+            const size_t kstride = (size_t)(d.L + 2) * n;
+            int s = 0;
+            u32 ph = 0;                                             // parity of the ring's current lap
+            int t = 0;
+            for (int bb = 0; bb < nb; bb++) {
+                const int b = b0 + bb;
+                const u64* key = keys[b];
+                const u64* er = E + (size_t)b * e_item_stride + (size_t)m * n + col0;
+                const u64* kbr = key + (size_t)pm * n + col0;
+                const u64* kar = key + (size_t)(d.L + 1) * kstride + (size_t)pm * n + col0;
+                for (int i = 0; i <= l; i++, t++) {
+                    if (t >= kKsi2Nst) mbar_wait(empty0 + 8 * s, ph ^ 1);
+                    const u32 full = full0 + 8 * s;
+                    const u32 dst = smb + (u32)(s * 3 * KSI2_ROWB);
+                    mbar_expect_tx(full, 3 * KSI2_ROWB);
+                    bulk_g2s(dst, er + (size_t)i * (l + 2) * n, KSI2_ROWB, full, pol_e);
+                    bulk_g2s(dst + KSI2_ROWB, kbr + (size_t)i * kstride, KSI2_ROWB, full, pol_k);
+                    bulk_g2s(dst + 2 * KSI2_ROWB, kar + (size_t)i * kstride, KSI2_ROWB, full, pol_k);
+                    if (++s == kKsi2Nst) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+        }
+        return;
+    }
+    // consumers
+    const PrimeConst P = d.pc[pm];
+    const u32 k = col0 + 2 * tid;
+    int s = 0;
+    u32 ph = 0;
+    for (int bb = 0; bb < nb; bb++) {
+        u64 lb0 = 0, hb0 = 0, la0 = 0, ha0 = 0, lb1 = 0, hb1 = 0, la1 = 0, ha1 = 0;
+        for (int i = 0; i <= l; i++) {
+            mbar_wait(full0 + 8 * s, ph);
+            const ulonglong2* row = (const ulonglong2*)(ksi2_smem + s * 3 * KSI2_ROWB);
+            const ulonglong2 ee = row[tid];
+            const ulonglong2 vb = row[KSI2_CT + tid];
+            const ulonglong2 va = row[2 * KSI2_CT + tid];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty0 + 8 * s);
+            if (++s == kKsi2Nst) {
+                s = 0;
+                ph ^= 1;
+            }
+            mac128(lb0, hb0, ee.x, vb.x);
+            mac128(lb1, hb1, ee.y, vb.y);
+            mac128(la0, ha0, ee.x, va.x);
+            mac128(la1, ha1, ee.y, va.y);
+        }
+        u64* out = ACC + (size_t)(b0 + bb) * 2 * (l + 2) * n;
+        *(ulonglong2*)(out + (size_t)m * n + k) = make_ulonglong2(reduce128(lb0, hb0, P), reduce128(lb1, hb1, P));
+        *(ulonglong2*)(out + ((size_t)(l + 2) + m) * n + k) =
+            make_ulonglong2(reduce128(la0, ha0, P), reduce128(la1, ha1, P));
+    }
+}
+
+// ks_inner over B un-permuted items: the bulk-async kernel when the ring has
+// whole 256-coefficient tiles (HS_KSI_LDG=1 selects the LDG kernel, A/B).
+static void launch_ks_inner(const Dev& d, int l, int B, const u64* E, size_t e_item_stride,
+                            const u64* const* keys, u64* ACC, cudaStream_t st) {
+    static const bool ldg = getenv("HS_KSI_LDG") != nullptr;
+    if (ldg || d.n % KSI2_C) {
+        ks_inner_kernel<<<ks_inner_grid(d, l, B), KSI_T, 0, st>>>(d, l, B, E, e_item_stride, keys, nullptr,
+                                                                 ACC);
+    } else {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(ks_inner_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)KSI2_SMEM);
+            attr = true;
+        }
+        const dim3 grid((B + kKsi2Ipb - 1) / kKsi2Ipb, d.n / KSI2_C, l + 2);
+        ks_inner_tma_kernel<<<grid, KSI2_CT + 32, KSI2_SMEM, st>>>(d, l, B, E, e_item_stride, keys, ACC);
+    }
+    note_launch();
+}
+
 // ModDown addends (what is added to the key-switch output), bound per CTA.
 struct AddNone {
     struct B {};
@@ -599,11 +760,8 @@ static void modup_and_inner(const Dev& d, int B, int l, u64* D, u64* E, const u6
         {
             ProbeScope ps(PROBE_KS_INNER, st, ks_inner_bytes(d, l, B, nkeys),
                           (double)B * 2 * (l + 1) * (l + 2) * n);
-            ks_inner_kernel<<<ks_inner_grid(d, l, B), KSI_T, 0, st>>>(d, l, B, E,
-                                                                     (size_t)(l + 1) * (l + 2) * d.n,
-                                                                     keys, nullptr, ACC);
+            launch_ks_inner(d, l, B, E, (size_t)(l + 1) * (l + 2) * d.n, keys, ACC, st);
         }
-        note_launch();
         return;
     }
     switch (d.log_n) {
