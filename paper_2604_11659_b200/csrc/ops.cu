@@ -441,11 +441,12 @@ HS_DEV void bulk_g2s(u32 dst, const void* src, u32 bytes, u32 bar, u64 policy) {
 
 __global__ void __launch_bounds__(KSI2_CT + 32)
 ks_inner_tma_kernel(Dev d, int l, int B, const u64* __restrict__ E, size_t e_item_stride,
-                    const u64* const* __restrict__ keys, u64* __restrict__ ACC) {
+                    const u64* const* __restrict__ keys, u64* __restrict__ ACC,
+                    const int* __restrict__ imap, int m0) {
     extern __shared__ __align__(128) unsigned char ksi2_smem[];
     __shared__ __align__(8) unsigned long long bars[2 * kKsi2Nst];     // full, empty
     const u32 n = d.n;
-    const int m = blockIdx.z;
+    const int m = m0 + (int)blockIdx.z;
     const u32 col0 = blockIdx.y * KSI2_C;
     const int b0 = blockIdx.x * kKsi2Ipb;
     const int nb = min(kKsi2Ipb, B - b0);
@@ -471,7 +472,7 @@ ks_inner_tma_kernel(Dev d, int l, int B, const u64* __restrict__ E, size_t e_ite
             u32 ph = 0;                                             // parity of the ring's current lap
             int t = 0;
             for (int bb = 0; bb < nb; bb++) {
-                const int b = b0 + bb;
+                const int b = imap ? imap[b0 + bb] : b0 + bb;         // physical item slot
                 const u64* key = keys[b];
                 const u64* er = E + (size_t)b * e_item_stride + (size_t)m * n + col0;
                 const u64* kbr = key + (size_t)pm * n + col0;
@@ -517,7 +518,8 @@ ks_inner_tma_kernel(Dev d, int l, int B, const u64* __restrict__ E, size_t e_ite
             mac128(la0, ha0, ee.x, va.x);
             mac128(la1, ha1, ee.y, va.y);
         }
-        u64* out = ACC + (size_t)(b0 + bb) * 2 * (l + 2) * n;
+        const int b = imap ? imap[b0 + bb] : b0 + bb;
+        u64* out = ACC + (size_t)b * 2 * (l + 2) * n;
         *(ulonglong2*)(out + (size_t)m * n + k) = make_ulonglong2(reduce128(lb0, hb0, P), reduce128(lb1, hb1, P));
         *(ulonglong2*)(out + ((size_t)(l + 2) + m) * n + k) =
             make_ulonglong2(reduce128(la0, ha0, P), reduce128(la1, ha1, P));
@@ -526,10 +528,18 @@ ks_inner_tma_kernel(Dev d, int l, int B, const u64* __restrict__ E, size_t e_ite
 
 // ks_inner over B un-permuted items: the bulk-async kernel when the ring has
 // whole 256-coefficient tiles (HS_KSI_LDG=1 selects the LDG kernel, A/B).
-static void launch_ks_inner(const Dev& d, int l, int B, const u64* E, size_t e_item_stride,
-                            const u64* const* keys, u64* ACC, cudaStream_t st) {
+// imap (device, optional): logical item -> physical item slot (E, keys, ACC);
+// targets m0 .. m0+mcnt-1 (default: all l+2).  Only the bulk-async kernel
+// takes imap / a target subset.
+static bool ks_inner_tma_ok(const Dev& d) {
     static const bool ldg = getenv("HS_KSI_LDG") != nullptr;
-    if (ldg || d.n % KSI2_C) {
+    return !ldg && d.n % KSI2_C == 0;
+}
+static void launch_ks_inner(const Dev& d, int l, int B, const u64* E, size_t e_item_stride,
+                            const u64* const* keys, u64* ACC, cudaStream_t st,
+                            const int* imap = nullptr, int m0 = 0, int mcnt = -1) {
+    if (mcnt < 0) mcnt = l + 2;
+    if (!ks_inner_tma_ok(d)) {
         ks_inner_kernel<<<ks_inner_grid(d, l, B), KSI_T, 0, st>>>(d, l, B, E, e_item_stride, keys, nullptr,
                                                                  ACC);
     } else {
@@ -539,8 +549,9 @@ static void launch_ks_inner(const Dev& d, int l, int B, const u64* E, size_t e_i
                                  (int)KSI2_SMEM);
             attr = true;
         }
-        const dim3 grid((B + kKsi2Ipb - 1) / kKsi2Ipb, d.n / KSI2_C, l + 2);
-        ks_inner_tma_kernel<<<grid, KSI2_CT + 32, KSI2_SMEM, st>>>(d, l, B, E, e_item_stride, keys, ACC);
+        const dim3 grid((B + kKsi2Ipb - 1) / kKsi2Ipb, d.n / KSI2_C, mcnt);
+        ks_inner_tma_kernel<<<grid, KSI2_CT + 32, KSI2_SMEM, st>>>(d, l, B, E, e_item_stride, keys, ACC,
+                                                                   imap, m0);
     }
     note_launch();
 }
@@ -934,7 +945,8 @@ void rotate_batch(const Dev& d, int B, int l, ItemPtr ct, const u32* gal, const 
 // ModDown epilogue, overwriting acc (its scratch between the two passes).
 __global__ void __launch_bounds__(256)
 rot_partial_kernel(Dev d, int B, int l, int chunk, ItemPtr ct, const u32* __restrict__ gal,
-                   const u64* __restrict__ ACC, const u64* __restrict__ T, u64* __restrict__ part) {
+                   const u64* __restrict__ ACC, const u64* __restrict__ T, u64* __restrict__ part,
+                   const unsigned char* __restrict__ head) {
     const u32 n = d.n;
     const u32 k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
@@ -944,9 +956,11 @@ rot_partial_kernel(Dev d, int B, int l, int chunk, ItemPtr ct, const u32* __rest
     const size_t acc_item = (size_t)2 * (l + 2) * n;
     u64 s0 = 0, s1 = 0, a0 = 0, z0 = 0, z1 = 0;
     for (int b = b0; b < b1; b++) {
-        const u64* A = ACC + (size_t)b * acc_item + (size_t)m * n + k;
-        s0 = add_mod(s0, __ldg(A), P.q);
-        s1 = add_mod(s1, __ldg(A + (size_t)(l + 2) * n), P.q);
+        if (!head || head[b]) {            // grouped: the head slot holds its group's sum
+            const u64* A = ACC + (size_t)b * acc_item + (size_t)m * n + k;
+            s0 = add_mod(s0, __ldg(A), P.q);
+            s1 = add_mod(s1, __ldg(A + (size_t)(l + 2) * n), P.q);
+        }
         a0 = add_mod(a0, __ldg(ct.at(b) + (size_t)m * n + galois_perm(k, gal[b], d.log_n)), P.q);
         z0 = add_mod(z0, lift_mod(__ldg(T + (size_t)b * 2 * n + k), d.aux_q, P), P.q);
         z1 = add_mod(z1, lift_mod(__ldg(T + ((size_t)b * 2 + 1) * n + k), d.aux_q, P), P.q);
@@ -1016,7 +1030,138 @@ bool rotate_accumulate(const Dev& d, int B, int l, ItemPtr ct, const u32* gal, c
     cudaMemsetAsync(F, 0, 2 * ls * sizeof(u64), st);
     cudaMemcpyAsync(F + 2 * ls, acc, 2 * ls * sizeof(u64), cudaMemcpyDeviceToDevice, st);
     cudaMemsetAsync(F + 4 * ls, 0, 2 * ls * sizeof(u64), st);
-    rot_partial_kernel<<<dim3((n + 255) / 256, nl, nchunks), 256, 0, st>>>(d, B, l, chunk, ct, gal, ACC, T, part);
+    rot_partial_kernel<<<dim3((n + 255) / 256, nl, nchunks), 256, 0, st>>>(d, B, l, chunk, ct, gal, ACC, T, part,
+                                                                         nullptr);
+    accum_fold_kernel<<<dim3((n + 255) / 256, 6 * nl), 256, 0, st>>>(d, nl, nchunks, part, F);
+    note_launch(2);
+    launch_ntt<true>(d, JobRotAcc{F, acc, l, d}, 2 * nl, st);
+    return true;
+}
+
+// ---- rotate-and-accumulate with items grouped by key.
+// Items [0, B) are sorted by rotation step, so the items sharing a Galois key
+// form runs (groups gs[g] .. gs[g+1]-1).  Only the SUM over items of the
+// rotated cts is needed, and for every chain modulus m <= l everything after
+// the digits' lifts is linear:
+//   sum_b acc_b,m = sum_i NTT_m(sum_b lift_m(x_b,i)) * K_g[i][m]   (m != i)
+//                 + (sum_b x_b,i df_i) * K_g[i][i]                 (m == i)
+// so the ModUp NTTs and the inner product of a chain modulus run once per
+// group (into the group head's slots), not once per item.  The aux modulus
+// stays per item: ModDown lifts T_b = INTT_p(acc_b,p) item by item (a
+// non-linear step), so each item keeps its own aux digit transforms and aux
+// accumulator.  Exact identities mod q_m: the residues equal the per-item
+// rotations summed (the reference's eval_rotate + eval_add).
+struct JobModUpGroup {                       // forward NTT, job = (g*(l+1)+i)*l + t
+    const u64* D;
+    u64* E;
+    const int* gs;                           // [G+1] group starts (items)
+    int l;
+    u32 n;
+    const PrimeConst* pc;
+    struct Ctx {
+        const u64* d;        // D[b0][i]
+        u64* e;              // E[b0][i][m]
+        size_t dstride;      // one item of D
+        u64 qsrc;
+        int cnt, pm;
+    };
+    HS_DEV Ctx make(int jb) const {
+        const int t = jb % l, gi = jb / l;
+        const int i = gi % (l + 1), g = gi / (l + 1);
+        const int m = t < i ? t : t + 1;     // m in [0, l] \ {i}
+        const int b0 = gs[g];
+        return Ctx{D + ((size_t)b0 * (l + 1) + i) * n, E + (((size_t)b0 * (l + 1) + i) * (l + 2) + m) * n,
+                   (size_t)(l + 1) * n, pc[i].q, gs[g + 1] - b0, m};
+    }
+    HS_DEV int prime(const Ctx& c) const { return c.pm; }
+    HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst& P) const {
+        u64 acc = lift_mod(__ldg(c.d + j), c.qsrc, P);
+        for (int k = 1; k < c.cnt; k++) acc = add_mod(acc, lift_mod(__ldg(c.d + k * c.dstride + j), c.qsrc, P), P.q);
+        return acc;
+    }
+    HS_DEV u64* scratch(const Ctx& c) const { return c.e; }
+    HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst&) const { c.e[j] = v; }   // [0, 4q)
+};
+
+struct JobModUpAux {                         // forward NTT, job = b*(l+1)+i: the aux target only
+    const u64* D;
+    u64* E;
+    int l, L;
+    u32 n;
+    const PrimeConst* pc;
+    struct Ctx {
+        const u64* d;
+        u64* e;
+        u64 qsrc;
+    };
+    HS_DEV Ctx make(int jb) const {
+        const int i = jb % (l + 1);
+        return Ctx{D + (size_t)jb * n, E + ((size_t)jb * (l + 2) + l + 1) * n, pc[i].q};
+    }
+    HS_DEV int prime(const Ctx&) const { return L + 1; }
+    HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst& P) const { return lift_mod(__ldg(c.d + j), c.qsrc, P); }
+    HS_DEV u64* scratch(const Ctx& c) const { return c.e; }
+    HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst&) const { c.e[j] = v; }
+};
+
+// E[b0][i][i] = sum over the group of E[b][i][i] (x_b,i df_i, canonical).
+__global__ void __launch_bounds__(256) group_diag_kernel(Dev d, int l, const int* __restrict__ gs, u64* E) {
+    const u32 n = d.n;
+    const u32 k = blockIdx.x * 256 + threadIdx.x;
+    const int i = blockIdx.y, g = blockIdx.z;
+    const int b0 = gs[g], b1 = gs[g + 1];
+    if (k >= n || b1 - b0 < 2) return;
+    const u64 q = d.pc[i].q;
+    const size_t item = (size_t)(l + 1) * (l + 2) * n, o = ((size_t)i * (l + 2) + i) * n + k;
+    u64 acc = E[(size_t)b0 * item + o];
+    for (int b = b0 + 1; b < b1; b++) acc = add_mod(acc, __ldg(E + (size_t)b * item + o), q);
+    E[(size_t)b0 * item + o] = acc;
+}
+
+bool rotate_accumulate_grouped(const Dev& d, int B, int G, const int* gs, const unsigned char* head, int l,
+                               ItemPtr ct, const u32* gal, const u64* const* keys, u64* acc, u64* scratch,
+                               cudaStream_t st) {
+    const u32 n = d.n;
+    const int nl = l + 1;
+    const size_t ls = (size_t)nl * n;
+    const long cap = (long)((size_t)B * (l + 1) * (l + 2) * n / (6 * ls)) - 1;
+    if (B <= 0 || G <= 0 || cap < 1 || !ks_inner_tma_ok(d) || l < 1) return false;
+    u64* E = scratch;
+    u64* D = E + (size_t)B * (l + 1) * (l + 2) * n;
+    u64* ACC = D + (size_t)B * (l + 1) * n;
+    u64* T = ACC + (size_t)B * 2 * (l + 2) * n;
+    const size_t e_item = (size_t)(l + 1) * (l + 2) * n;
+    launch_ntt<false>(d, JobDecompose<SrcPerm>{SrcPerm{ct, gal}, E, D, d.df, l, n, d}, B * (l + 1), st);
+    {
+        const double jobs = (double)G * (l + 1) * l + (double)B * (l + 1), nn = n;
+        ProbeScope ps(PROBE_MODUP, st, jobs * 32.0 * nn, jobs * (nn / 2) * d.log_n, 4);
+        launch_ntt<true>(d, JobModUpGroup{D, E, gs, l, n, d.pc}, G * (l + 1) * l, st);
+        launch_ntt<true>(d, JobModUpAux{D, E, l, d.L, n, d.pc}, B * (l + 1), st);
+    }
+    group_diag_kernel<<<dim3((n + 255) / 256, l + 1, G), 256, 0, st>>>(d, l, gs, E);
+    note_launch();
+    {
+        const double limb = 8.0 * n;
+        const double bytes = (double)G * (l + 1) * (l + 1) * limb + (double)B * (l + 1) * limb +
+                             (double)G * 2 * (l + 1) * (l + 2) * limb + (double)B * 2 * (l + 2) * limb;
+        ProbeScope ps(PROBE_KS_INNER, st, bytes, 2.0 * ((double)G * (l + 1) * (l + 1) + (double)B * (l + 1)) * n, 2);
+        launch_ks_inner(d, l, G, E, e_item, keys, ACC, st, gs, 0, l + 1);     // chain moduli, per group
+        launch_ks_inner(d, l, B, E, e_item, keys, ACC, st, nullptr, l + 1, 1); // aux modulus, per item
+    }
+    launch_ntt<false>(d, JobInvGather{strided(ACC, (size_t)(l + 2) * n), 1, l + 2, l + 1, d.L + 1, T, n},
+                      B * 2, st);
+    const int cols = (int)((n + 255) / 256) * nl;
+    int nchunks = std::max(1, std::min((B + 7) / 8, (148 * 8 + cols - 1) / cols));
+    nchunks = (int)std::min<long>(nchunks, cap);
+    const int chunk = (B + nchunks - 1) / nchunks;
+    nchunks = (B + chunk - 1) / chunk;
+    u64* F = E;
+    u64* part = F + 6 * ls;
+    cudaMemsetAsync(F, 0, 2 * ls * sizeof(u64), st);
+    cudaMemcpyAsync(F + 2 * ls, acc, 2 * ls * sizeof(u64), cudaMemcpyDeviceToDevice, st);
+    cudaMemsetAsync(F + 4 * ls, 0, 2 * ls * sizeof(u64), st);
+    rot_partial_kernel<<<dim3((n + 255) / 256, nl, nchunks), 256, 0, st>>>(d, B, l, chunk, ct, gal, ACC, T, part,
+                                                                         head);
     accum_fold_kernel<<<dim3((n + 255) / 256, 6 * nl), 256, 0, st>>>(d, nl, nchunks, part, F);
     note_launch(2);
     launch_ntt<true>(d, JobRotAcc{F, acc, l, d}, 2 * nl, st);

@@ -71,6 +71,12 @@ void rotate_batch(const Dev& d, int B, int l, ItemPtr ct, const u32* gal, const 
 // output limb); false (nothing launched) when the scratch is too small.
 bool rotate_accumulate(const Dev& d, int B, int l, ItemPtr ct, const u32* gal, const u64* const* keys,
                        u64* acc, u64* scratch, cudaStream_t st, int nkeys);
+// Same, items sorted by key in G runs: gs[0..G] (device) = run starts,
+// head[b] (device) = 1 for the first item of a run.  ModUp and the inner
+// product of the chain moduli run once per run (SURVEY P4 + linearity).
+bool rotate_accumulate_grouped(const Dev& d, int B, int G, const int* gs, const unsigned char* head, int l,
+                               ItemPtr ct, const u32* gal, const u64* const* keys, u64* acc, u64* scratch,
+                               cudaStream_t st);
 // Hoisted rotations of ONE source ct into R outputs (one per step).
 void rotate_hoisted(const Dev& d, int R, int l, const u64* src, const u32* gal,
                     const u64* const* keys, ItemPtr out, u64* scratch, cudaStream_t st);

@@ -443,6 +443,18 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, cons
 
     std::vector<u32> hR(P);
     for (int64_t t = 0; t < P; t++) hR[t] = accr[order[lo + t]];
+    // key runs of each batch's rotated items (rotate_accumulate_grouped):
+    // group starts relative to the batch's first rotated item, and head flags;
+    // host arrays stay alive (and distinct per batch) for the async copies
+    static const bool no_group = getenv("HS_NO_GROUP_ROT") != nullptr;   // A/B knob
+    std::vector<int> hGS(2 * P + 2);
+    std::vector<unsigned char> hHead(P);
+    int* dGS = A.get<int>(2 * P + 2);
+    unsigned char* dHead = A.get<unsigned char>(P);
+    if (A.failed) {
+        set_error("out of device memory (group tables)");
+        return (hs_status)HS_OUT_OF_MEMORY;
+    }
     // batches: up to B pairs and at most max_gen distinct non-resident keys
     std::vector<int64_t> bstart;
     std::vector<std::vector<u32>> bsteps_all;
@@ -503,9 +515,28 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, cons
         // accumulation rotations (step-0 pairs form the sorted prefix)
         accumulate(d, z, L - 1, 2, strided(Cb, ctL2), out, st);
         static const bool split_rot = getenv("HS_SPLIT_ROTATE_ACCUM") != nullptr;
-        if (bn - z > 0 && (split_rot || !rotate_accumulate(d, bn - z, L - 2, strided(Cb + (size_t)z * ctL2, ctL2),
-                                                           dG + s + z, dK + s + z, out, ks, st,
-                                                           (int)bsteps.size()))) {
+        bool done = false;
+        const int nr = bn - z;
+        if (nr > 0 && !split_rot && !no_group && (int)bsteps.size() < nr) {
+            // runs of equal steps among the rotated items [s+z, bnext)
+            int* gsh = hGS.data() + (s + z) + bi;              // distinct slice per batch
+            int G = 0;
+            for (int t = 0; t < nr; t++) {
+                const bool h = t == 0 || hR[s + z + t] != hR[s + z + t - 1];
+                hHead[s + z + t] = h;
+                if (h) gsh[G++] = t;
+            }
+            gsh[G] = nr;
+            int* dgs = dGS + (gsh - hGS.data());
+            HS_CUDA(cudaMemcpyAsync(dgs, gsh, (G + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
+            HS_CUDA(cudaMemcpyAsync(dHead + s + z, hHead.data() + s + z, nr, cudaMemcpyHostToDevice, st));
+            done = rotate_accumulate_grouped(d, nr, G, dgs, dHead + s + z, L - 2,
+                                             strided(Cb + (size_t)z * ctL2, ctL2), dG + s + z, dK + s + z, out,
+                                             ks, st);
+        }
+        if (nr > 0 && !done && (split_rot || !rotate_accumulate(d, nr, L - 2, strided(Cb + (size_t)z * ctL2, ctL2),
+                                                                 dG + s + z, dK + s + z, out, ks, st,
+                                                                 (int)bsteps.size()))) {
             rotate_batch(d, bn - z, L - 2, strided(Cb + (size_t)z * ctL2, ctL2), dG + s + z, dK + s + z,
                          strided(Fb + (size_t)z * ctL2, ctL2), ks, st);
             accumulate(d, bn - z, L - 1, 2, strided(Fb + (size_t)z * ctL2, ctL2), out, st);

@@ -5,6 +5,8 @@ rescale, the top-limb INTT, rotate-and-accumulate with one ModDown NTT per
 output limb).  Each merge has an environment switch back to the plain
 sequence (read once per process), so every combination is run in its own
 process on the same seeded product and must give the same ciphertext bits.
+HS_NO_GROUP_ROT turns off the per-key-group ModUp/inner product of the
+accumulation rotations, HS_KSI_LDG the bulk-async inner-product kernel.
 The default path itself is checked against the oracle and the golden
 vectors in test_gpu_parity.py.
 """
@@ -34,7 +36,8 @@ for (n, sb, L, seed, dim, sp, mseed) in [(8192, 45, 4, 2024, 12, 0.6, 5), (16384
 print("DIGESTS " + json.dumps(out))
 """
 
-SWITCHES = ["HS_SPLIT_MODDOWN_RESCALE", "HS_TOPLIMB_FWD", "HS_SPLIT_ROTATE_ACCUM"]
+SWITCHES = ["HS_SPLIT_MODDOWN_RESCALE", "HS_TOPLIMB_FWD", "HS_SPLIT_ROTATE_ACCUM", "HS_NO_GROUP_ROT",
+            "HS_KSI_LDG"]
 
 
 def _digests(env_on):
@@ -52,5 +55,6 @@ def _digests(env_on):
 
 def test_merged_sequences_equal_plain_sequences():
     base = _digests([])
-    for on in (["HS_SPLIT_MODDOWN_RESCALE"], ["HS_TOPLIMB_FWD"], ["HS_SPLIT_ROTATE_ACCUM"], SWITCHES):
+    for on in (["HS_SPLIT_MODDOWN_RESCALE"], ["HS_TOPLIMB_FWD"], ["HS_SPLIT_ROTATE_ACCUM"],
+               ["HS_NO_GROUP_ROT"], ["HS_KSI_LDG"], SWITCHES):
         assert _digests(on) == base, on
