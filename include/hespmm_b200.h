@@ -213,6 +213,21 @@ hs_status hs_spmspm_pairs(hs_ctx* ctx, int32_t dim, const int64_t* pairs, int64_
                           const uint64_t* const* masks, int64_t nmasks, uint64_t* out,
                           hs_counters* counters, int32_t shard_index, int32_t shard_count,
                           void* stream);
+
+/* Alignment rotations shared across ranks (multi-GPU, dist.py).  The CSR/C
+ * runner rotates the higher-positioned operand of a pair by |a_pos - b_pos|
+ * (engine.py:136-160); each distinct (operand, step) is one hoisted rotation
+ * of ct_a (operand 0) or ct_b (operand 1) at level L.
+ * hs_align_compute: those rotations for count (operand, normalised step)
+ * entries into outs[k] (device buffers [2][L+1][n]); Galois keys resident or
+ * lazily registered.  hs_align_provide: hand the runner aligned operands
+ * another rank computed (device pointers, valid until hs_align_clear); the
+ * runner then uses them instead of computing those rotations. */
+hs_status hs_align_compute(hs_ctx* ctx, const uint64_t* ct_a, const uint64_t* ct_b, const int32_t* operand,
+                           const uint32_t* steps, int64_t count, uint64_t* const* outs, void* stream);
+hs_status hs_align_provide(hs_ctx* ctx, const int32_t* operand, const uint32_t* steps,
+                           const uint64_t* const* cts, int64_t count);
+void hs_align_clear(hs_ctx* ctx);
 /* Final modular reduction after an integer SUM collective of shard results
  * (shard_count * q < 2^63, so an int64 NCCL sum is exact). */
 hs_status hs_reduce_mod(hs_ctx* ctx, uint64_t* data, int32_t npoly, int32_t nlimbs, void* stream);

@@ -94,6 +94,13 @@ _SIGS = {
                                        c_vp]),
     "hs_reduce_mod": (ctypes.c_int, [c_vp, c_vp, ctypes.c_int32, ctypes.c_int32, c_vp]),
     "hs_set_batch_bytes": (None, [c_vp, ctypes.c_uint64]),
+    "hs_align_compute": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.POINTER(ctypes.c_int32),
+                                        ctypes.POINTER(ctypes.c_uint32), ctypes.c_int64,
+                                        ctypes.POINTER(c_vp), c_vp]),
+    "hs_align_provide": (ctypes.c_int, [c_vp, ctypes.POINTER(ctypes.c_int32),
+                                        ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(c_vp),
+                                        ctypes.c_int64]),
+    "hs_align_clear": (None, [c_vp]),
 }
 
 EXPORTS = tuple(_SIGS)

@@ -57,6 +57,8 @@ struct hs_ctx {
     ulonglong2* d_kskf = nullptr;            // p (Q_L/q_i) mod q_m, Shoup pairs [(L+1)^2]
     struct Stream { u64 s_hi, s_lo, i_hi, i_lo; };
     std::unordered_map<u32, Stream> lazy;    // registered steps generated on demand
+    // aligned operands computed elsewhere (another rank), key = operand * n/2 + step
+    std::unordered_map<u64, const u64*> ext_align;
     size_t keygen_batch = 64;                // keys generated per launch (per-launch latency amortised)
     int64_t keys_generated = 0;
     int* d_kg_err = nullptr;                 // set if a keygen stream window overflowed

@@ -1052,32 +1052,30 @@ bool rotate_accumulate(const Dev& d, int B, int l, ItemPtr ct, const u32* gal, c
 // accumulator.  Exact identities mod q_m: the residues equal the per-item
 // rotations summed (the reference's eval_rotate + eval_add).
 struct JobModUpGroup {                       // forward NTT, job = (g*(l+1)+i)*l + t
-    const u64* D;
+    const u64* D;                            // head slot of each group: signed sum (group_sum_kernel)
     u64* E;
     const int* gs;                           // [G+1] group starts (items)
     int l;
     u32 n;
     const PrimeConst* pc;
     struct Ctx {
-        const u64* d;        // D[b0][i]
+        const u64* d;        // D[b0][i]: sum over the group of the centred digits (int64)
         u64* e;              // E[b0][i][m]
-        size_t dstride;      // one item of D
-        u64 qsrc;
-        int cnt, pm;
+        int pm;
     };
     HS_DEV Ctx make(int jb) const {
         const int t = jb % l, gi = jb / l;
         const int i = gi % (l + 1), g = gi / (l + 1);
         const int m = t < i ? t : t + 1;     // m in [0, l] \ {i}
         const int b0 = gs[g];
-        return Ctx{D + ((size_t)b0 * (l + 1) + i) * n, E + (((size_t)b0 * (l + 1) + i) * (l + 2) + m) * n,
-                   (size_t)(l + 1) * n, pc[i].q, gs[g + 1] - b0, m};
+        return Ctx{D + ((size_t)b0 * (l + 1) + i) * n, E + (((size_t)b0 * (l + 1) + i) * (l + 2) + m) * n, m};
     }
     HS_DEV int prime(const Ctx& c) const { return c.pm; }
+    // sum_b lift_m(x_b) = (sum_b centred(x_b)) mod q_m: one signed reduction
     HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst& P) const {
-        u64 acc = lift_mod(__ldg(c.d + j), c.qsrc, P);
-        for (int k = 1; k < c.cnt; k++) acc = add_mod(acc, lift_mod(__ldg(c.d + k * c.dstride + j), c.qsrc, P), P.q);
-        return acc;
+        const long long v = (long long)__ldg(c.d + j);
+        const u64 t = reduce64(v < 0 ? 0ull - (u64)v : (u64)v, P);
+        return (v < 0 && t) ? P.q - t : t;
     }
     HS_DEV u64* scratch(const Ctx& c) const { return c.e; }
     HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst&) const { c.e[j] = v; }   // [0, 4q)
@@ -1104,14 +1102,26 @@ struct JobModUpAux {                         // forward NTT, job = b*(l+1)+i: th
     HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst&) const { c.e[j] = v; }
 };
 
-// E[b0][i][i] = sum over the group of E[b][i][i] (x_b,i df_i, canonical).
-__global__ void __launch_bounds__(256) group_diag_kernel(Dev d, int l, const int* __restrict__ gs, u64* E) {
+// Per group and digit i: D[b0][i] := sum_b centred(x_b,i) as int64 (|sum| <
+// 16 q_i / 2 < 2^63 with at most 16 items per group), and
+// E[b0][i][i] := sum_b E[b][i][i] (x_b,i df_i, canonical).  Runs after the
+// per-item aux ModUp, which still reads every item's own digit.
+__global__ void __launch_bounds__(256) group_sum_kernel(Dev d, int l, const int* __restrict__ gs, u64* D,
+                                                        u64* E) {
     const u32 n = d.n;
     const u32 k = blockIdx.x * 256 + threadIdx.x;
     const int i = blockIdx.y, g = blockIdx.z;
     const int b0 = gs[g], b1 = gs[g + 1];
-    if (k >= n || b1 - b0 < 2) return;
-    const u64 q = d.pc[i].q;
+    if (k >= n) return;
+    const u64 q = d.pc[i].q, half = q >> 1;
+    const size_t ditem = (size_t)(l + 1) * n, od = (size_t)i * n + k;
+    long long sum = 0;
+    for (int b = b0; b < b1; b++) {
+        const u64 x = D[(size_t)b * ditem + od];
+        sum += x > half ? (long long)x - (long long)q : (long long)x;
+    }
+    D[(size_t)b0 * ditem + od] = (u64)sum;
+    if (b1 - b0 < 2) return;
     const size_t item = (size_t)(l + 1) * (l + 2) * n, o = ((size_t)i * (l + 2) + i) * n + k;
     u64 acc = E[(size_t)b0 * item + o];
     for (int b = b0 + 1; b < b1; b++) acc = add_mod(acc, __ldg(E + (size_t)b * item + o), q);
@@ -1135,11 +1145,11 @@ bool rotate_accumulate_grouped(const Dev& d, int B, int G, const int* gs, const 
     {
         const double jobs = (double)G * (l + 1) * l + (double)B * (l + 1), nn = n;
         ProbeScope ps(PROBE_MODUP, st, jobs * 32.0 * nn, jobs * (nn / 2) * d.log_n, 4);
-        launch_ntt<true>(d, JobModUpGroup{D, E, gs, l, n, d.pc}, G * (l + 1) * l, st);
         launch_ntt<true>(d, JobModUpAux{D, E, l, d.L, n, d.pc}, B * (l + 1), st);
+        group_sum_kernel<<<dim3((n + 255) / 256, l + 1, G), 256, 0, st>>>(d, l, gs, D, E);
+        note_launch();
+        launch_ntt<true>(d, JobModUpGroup{D, E, gs, l, n, d.pc}, G * (l + 1) * l, st);
     }
-    group_diag_kernel<<<dim3((n + 255) / 256, l + 1, G), 256, 0, st>>>(d, l, gs, E);
-    note_launch();
     {
         const double limb = 8.0 * n;
         const double bytes = (double)G * (l + 1) * (l + 1) * limb + (double)B * (l + 1) * limb +

@@ -218,6 +218,69 @@ struct KeyProvider {
     }
 };
 
+// Hoisted alignment rotations: todo[k] = (source operand 0|1, normalised
+// step) rotated at level L into outs[k]; per source one decomposition + ModUp
+// per chunk of steps (chunks bounded by the work budget and, for generated
+// keys, by the key pool).
+static hs_status compute_alignments(hs_ctx* c, const u64* ct_a, const u64* ct_b,
+                                    const std::vector<std::pair<int, u32>>& todo,
+                                    const std::vector<u64*>& outs_all, KeyProvider& KP, DeviceArena& A,
+                                    size_t budget, int64_t max_gen, cudaStream_t st) {
+    const int L = c->L;
+    const u32 n = c->n;
+    const Dev& d = c->dev;
+    for (int src = 0; src < 2; src++) {
+        std::vector<u32> gal, steps_src;
+        std::vector<const u64*> keys;
+        std::vector<const u64*> outs;
+        for (size_t k = 0; k < todo.size(); k++) {
+            const auto& al = todo[k];
+            if (al.first != src) continue;
+            gal.push_back((u32)powmod_h(5, al.second, 2ull * n));
+            steps_src.push_back(al.second);
+            outs.push_back(outs_all[k]);
+        }
+        keys.assign(gal.size(), nullptr);
+        const int R = (int)gal.size();
+        if (!R) continue;
+        const size_t base_e = ks_hoisted_scratch_elems(0, L, n);
+        const size_t per_e = ks_hoisted_scratch_elems(1, L, n) - base_e;
+        int64_t rmax = budget / 8 > base_e ? (int64_t)((budget / 8 - base_e) / per_e) : 1;
+        rmax = std::max<int64_t>(1, std::min<int64_t>(rmax, R));
+        bool any_gen = false;
+        for (u32 r : steps_src) any_gen |= !KP.resident(r);
+        if (any_gen) rmax = std::min<int64_t>(rmax, max_gen);
+        u64* scratch = A.get<u64>(ks_hoisted_scratch_elems((int)rmax, L, n));
+        u32* d_gal = A.get<u32>(R);
+        const u64** d_keys = A.get<const u64*>(R);
+        const u64** d_outs = A.get<const u64*>(R);
+        if (A.failed) {
+            set_error("out of device memory (alignment)");
+            return (hs_status)HS_OUT_OF_MEMORY;
+        }
+        HS_CUDA(cudaMemcpyAsync(d_gal, gal.data(), R * sizeof(u32), cudaMemcpyHostToDevice, st));
+        HS_CUDA(cudaMemcpyAsync(d_outs, outs.data(), R * sizeof(u64*), cudaMemcpyHostToDevice, st));
+        const u64* sp = src ? ct_b : ct_a;
+        for (int r0 = 0; r0 < R; r0 += (int)rmax) {
+            const int rc = std::min<int>((int)rmax, R - r0);
+            std::vector<u32> chunk(steps_src.begin() + r0, steps_src.begin() + r0 + rc);
+            std::vector<const u64*> kp;
+            hs_status ks_ = KP.acquire(chunk, kp);
+            if (ks_ != HS_OK) return ks_;
+            if (any_gen && r0 + rc < R && prefetch_on()) {   // next chunk's keys while this one computes
+                const int rn = std::min<int>((int)rmax, R - r0 - rc);
+                ks_ = KP.prefetch(std::vector<u32>(steps_src.begin() + r0 + rc,
+                                                   steps_src.begin() + r0 + rc + rn), chunk);
+                if (ks_ != HS_OK) return ks_;
+            }
+            HS_CUDA(cudaMemcpyAsync(d_keys + r0, kp.data(), rc * sizeof(u64*), cudaMemcpyHostToDevice, st));
+            rotate_hoisted(d, rc, L, sp, d_gal + r0, d_keys + r0, table(d_outs + r0), scratch, st);
+            KP.release(chunk);
+        }
+    }
+    return HS_OK;
+}
+
 hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, const u64* ct_a,
                     const u64* ct_b, const u64* const* masks, int64_t nmasks, u64* out,
                     hs_counters* cnt, int shard, int nshard, cudaStream_t st,
@@ -312,16 +375,15 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, cons
     C.pairs = P;
 
     // alignments this shard needs, compacted
-    std::vector<int32_t> slot_of(2 + align_list.size(), -1);
+    std::vector<char> seen(2 + align_list.size(), 0);
     std::vector<int32_t> need;
     for (int64_t t = lo; t < hi; t++) {
         for (int32_t idx : {ia[order[t]], ib[order[t]]})
-            if (idx >= 2 && slot_of[idx] < 0) {
-                slot_of[idx] = (int32_t)need.size();
+            if (idx >= 2 && !seen[idx]) {
+                seen[idx] = 1;
                 need.push_back(idx);
             }
     }
-    C.physical_alignment = (int64_t)need.size();
     const auto t_plan = std::chrono::steady_clock::now();
     C.plan_ms = std::chrono::duration<double, std::milli>(t_plan - t_start).count();
 
@@ -339,69 +401,43 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, cons
     // generated keys per chunk/batch: the key pool holds two such sets (the
     // one in use and the one being prefetched), bounded by twice the budget
     const int64_t max_gen = std::max<int64_t>(1, (int64_t)(budget / c->key_bytes()));
+
+    // ---- phase 1: hoisted alignment rotations (those another rank computed
+    // and handed over with hs_align_provide are used as they are)
+    std::vector<const u64*> align_ptr(2 + align_list.size(), nullptr);
+    std::vector<std::pair<int, u32>> todo;
+    std::vector<u64*> todo_out;
+    size_t n_local = 0;
+    for (int32_t idx : need) {
+        const auto& al = align_list[idx - 2];
+        auto it = c->ext_align.find((u64)al.first * slots + al.second);
+        if (it != c->ext_align.end()) align_ptr[idx] = it->second;
+        else n_local++;
+    }
+    u64* aligned = A.get<u64>(n_local * ctL);
+    if (A.failed) {
+        set_error("out of device memory for aligned operands");
+        return (hs_status)HS_OUT_OF_MEMORY;
+    }
+    for (int32_t idx : need) {
+        if (align_ptr[idx]) continue;
+        u64* o = aligned + todo.size() * ctL;
+        align_ptr[idx] = o;
+        todo.push_back(align_list[idx - 2]);
+        todo_out.push_back(o);
+    }
+    C.physical_alignment = (int64_t)todo.size();
     bool lazy_needed = false;
-    for (const auto& al : align_list) lazy_needed |= !c->galois.count(al.second);
+    for (const auto& al : todo) lazy_needed |= !c->galois.count(al.second);
     for (int64_t t = lo; t < hi && !lazy_needed; t++)
         lazy_needed |= accr[order[t]] && !c->galois.count(accr[order[t]]);
     if (lazy_needed) {
         hs_status ks_ = KP.init((int)(2 * max_gen));
         if (ks_ != HS_OK) return ks_;
     }
-
-    // ---- phase 1: hoisted alignment rotations
-    u64* aligned = A.get<u64>(need.size() * ctL);
-    if (A.failed) {
-        set_error("out of device memory for aligned operands");
-        return (hs_status)HS_OUT_OF_MEMORY;
-    }
-    for (int src = 0; src < 2; src++) {
-        std::vector<u32> gal, steps_src;
-        std::vector<const u64*> keys;
-        std::vector<const u64*> outs;
-        for (size_t k = 0; k < need.size(); k++) {
-            const auto& al = align_list[need[k] - 2];
-            if (al.first != src) continue;
-            gal.push_back((u32)powmod_h(5, al.second, 2ull * n));
-            steps_src.push_back(al.second);
-            outs.push_back(aligned + k * ctL);
-        }
-        keys.assign(gal.size(), nullptr);
-        const int R = (int)gal.size();
-        if (!R) continue;
-        const size_t base_e = ks_hoisted_scratch_elems(0, L, n);
-        const size_t per_e = ks_hoisted_scratch_elems(1, L, n) - base_e;
-        int64_t rmax = budget / 8 > base_e ? (int64_t)((budget / 8 - base_e) / per_e) : 1;
-        rmax = std::max<int64_t>(1, std::min<int64_t>(rmax, R));
-        bool any_gen = false;
-        for (u32 r : steps_src) any_gen |= !KP.resident(r);
-        if (any_gen) rmax = std::min<int64_t>(rmax, max_gen);
-        u64* scratch = A.get<u64>(ks_hoisted_scratch_elems((int)rmax, L, n));
-        u32* d_gal = A.get<u32>(R);
-        const u64** d_keys = A.get<const u64*>(R);
-        const u64** d_outs = A.get<const u64*>(R);
-        if (A.failed) {
-            set_error("out of device memory (alignment)");
-            return (hs_status)HS_OUT_OF_MEMORY;
-        }
-        HS_CUDA(cudaMemcpyAsync(d_gal, gal.data(), R * sizeof(u32), cudaMemcpyHostToDevice, st));
-        HS_CUDA(cudaMemcpyAsync(d_outs, outs.data(), R * sizeof(u64*), cudaMemcpyHostToDevice, st));
-        const u64* sp = src ? ct_b : ct_a;
-        for (int r0 = 0; r0 < R; r0 += (int)rmax) {
-            const int rc = std::min<int>((int)rmax, R - r0);
-            std::vector<u32> chunk(steps_src.begin() + r0, steps_src.begin() + r0 + rc);
-            std::vector<const u64*> kp;
-            hs_status ks_ = KP.acquire(chunk, kp);
-            if (ks_ != HS_OK) return ks_;
-            if (any_gen && r0 + rc < R && prefetch_on()) {   // next chunk's keys while this one computes
-                const int rn = std::min<int>((int)rmax, R - r0 - rc);
-                ks_ = KP.prefetch(std::vector<u32>(steps_src.begin() + r0 + rc,
-                                                   steps_src.begin() + r0 + rc + rn), chunk);
-                if (ks_ != HS_OK) return ks_;
-            }
-            HS_CUDA(cudaMemcpyAsync(d_keys + r0, kp.data(), rc * sizeof(u64*), cudaMemcpyHostToDevice, st));
-            rotate_hoisted(d, rc, L, sp, d_gal + r0, d_keys + r0, table(d_outs + r0), scratch, st);
-            KP.release(chunk);
-        }
+    {
+        hs_status s_ = compute_alignments(c, ct_a, ct_b, todo, todo_out, KP, A, budget, max_gen, st);
+        if (s_ != HS_OK) return s_;
     }
 
     // ---- phase 2: pair batches
@@ -409,8 +445,8 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, cons
     std::vector<u32> hG(P);
     for (int64_t t = 0; t < P; t++) {
         const int64_t p = order[lo + t];
-        hA[t] = ia[p] >= 2 ? aligned + (size_t)slot_of[ia[p]] * ctL : ct_a;
-        hB[t] = ib[p] >= 2 ? aligned + (size_t)slot_of[ib[p]] * ctL : ct_b;
+        hA[t] = ia[p] >= 2 ? align_ptr[ia[p]] : ct_a;
+        hB[t] = ib[p] >= 2 ? align_ptr[ib[p]] : ct_b;
         hM[t] = masks[mpos[p]];
         hG[t] = accr[p] ? (u32)powmod_h(5, accr[p], 2ull * n) : 0u;
     }
@@ -521,8 +557,10 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, cons
             // runs of equal steps among the rotated items [s+z, bnext)
             int* gsh = hGS.data() + (s + z) + bi;              // distinct slice per batch
             int G = 0;
-            for (int t = 0; t < nr; t++) {
-                const bool h = t == 0 || hR[s + z + t] != hR[s + z + t - 1];
+            for (int t = 0, run = 0; t < nr; t++) {
+                // at most 16 items per group: the group's digit sums stay exact in int64
+                const bool h = t == 0 || hR[s + z + t] != hR[s + z + t - 1] || run == 16;
+                run = h ? 1 : run + 1;
                 hHead[s + z + t] = h;
                 if (h) gsh[G++] = t;
             }
@@ -615,5 +653,62 @@ hs_status hs_reduce_mod(hs_ctx* c, uint64_t* data, int32_t npoly, int32_t nlimbs
 }
 
 void hs_set_batch_bytes(hs_ctx* c, uint64_t bytes) { c->batch_bytes = bytes; }
+
+hs_status hs_align_provide(hs_ctx* c, const int32_t* src, const uint32_t* steps, const uint64_t* const* cts,
+                           int64_t count) {
+    const u32 slots = c->n / 2;
+    for (int64_t k = 0; k < count; k++) {
+        if ((src[k] != 0 && src[k] != 1) || steps[k] == 0 || steps[k] >= slots) {
+            set_error("hs_align_provide: bad (operand, step)");
+            return HS_PARAMETER_ERROR;
+        }
+        c->ext_align[(u64)src[k] * slots + steps[k]] = cts[k];
+    }
+    return HS_OK;
+}
+
+void hs_align_clear(hs_ctx* c) { c->ext_align.clear(); }
+
+hs_status hs_align_compute(hs_ctx* c, const uint64_t* ct_a, const uint64_t* ct_b, const int32_t* src,
+                           const uint32_t* steps, int64_t count, uint64_t* const* outs, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    const u32 slots = c->n / 2;
+    std::vector<std::pair<int, u32>> todo;
+    std::vector<u64*> o(outs, outs + count);
+    bool lazy = false;
+    for (int64_t k = 0; k < count; k++) {
+        if ((src[k] != 0 && src[k] != 1) || steps[k] == 0 || steps[k] >= slots) {
+            set_error("hs_align_compute: bad (operand, step)");
+            return HS_PARAMETER_ERROR;
+        }
+        if (!c->galois.count(steps[k])) {
+            if (!c->lazy.count(steps[k])) {
+                set_error("missing Galois key for step " + std::to_string(steps[k]));
+                return HS_KEY_MISSING;
+            }
+            lazy = true;
+        }
+        todo.push_back({src[k], steps[k]});
+    }
+    DeviceArena A{st};
+    KeyProvider KP{c, st};
+    const int64_t max_gen = std::max<int64_t>(1, (int64_t)(c->batch_bytes / c->key_bytes()));
+    if (lazy) {
+        hs_status s = KP.init((int)(2 * max_gen));
+        if (s != HS_OK) return s;
+    }
+    hs_status s = compute_alignments(c, ct_a, ct_b, todo, o, KP, A, c->batch_bytes, max_gen, st);
+    if (s != HS_OK) return s;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error(std::string("kernel launch failed: ") + cudaGetErrorString(e));
+        return HS_CUDA_ERROR;
+    }
+    if (lazy) {
+        HS_CUDA(cudaStreamSynchronize(st));
+        return keygen_check(c);
+    }
+    return HS_OK;
+}
 
 }  // extern "C"
