@@ -1,11 +1,15 @@
-"""Multi-process (world_size 2, gloo, CPU) coverage of the multi-GPU combine.
+"""Multi-process (world_size 2 and 3, gloo, CPU) coverage of the multi-GPU path.
 
-On GPUs each rank executes one contiguous share of the step-sorted pair
-list and the partial result ciphertexts are summed with one integer
-all-reduce followed by a mod-q pass (paper_2604_11659_b200/dist.py).  Here
-each rank computes its share's partial with the CPU oracle, combines through
-the same ``reduce_partials`` over gloo, and must reproduce the single-process
-result bit for bit.
+On GPUs (paper_2604_11659_b200/dist.py) every rank runs the product's shard
+plan (``plan_shards``): one contiguous share of the step-sorted pair list,
+and ownership of a balanced subset of the distinct alignment rotations;
+owners compute their aligned operands and ``exchange_aligned`` ships them
+point-to-point to the ranks that need them; partial result ciphertexts are
+summed with one integer all-reduce (``reduce_partials``) and a mod-q pass.
+Here the same planner, exchange and all-reduce run over gloo; the CPU oracle
+(the checker) supplies the rotations and partial products, so every received
+aligned operand and the combined result must match the single-process
+oracle bit for bit.
 """
 
 import os
@@ -89,6 +93,63 @@ def test_sharded_partials_allreduce_to_single_process_result(world):
         assert p.exitcode == 0
     assert sum(g[2] for g in got) == len(pairs)
     for rank, blob, _ in got:
+        arr = np.frombuffer(blob, dtype=np.uint64).reshape(want.shape)
+        assert np.array_equal(arr, want), rank
+
+
+def _worker_owned(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2604_11659_b200.dist import exchange_aligned, host_mod, plan_shards, reduce_partials
+    P, ctx, keys, ca, cb, pairs, dim, masks = _case()
+    L = P.levels
+    plan = plan_shards(pairs, dim, P.slots, world)
+    src_ct = (ca, cb)
+
+    def rotated(a):
+        s, r = plan["align"][a]
+        return torch.from_numpy(ctx.eval_rotate(src_ct[s], r, keys.galois, L).view(np.int64).copy())
+
+    owned = {a: rotated(a) for a in range(len(plan["align"])) if plan["owner"][a] == rank}
+    got = exchange_aligned(plan, rank, world, owned,
+                           lambda: torch.zeros((2, L + 1, P.ring_degree), dtype=torch.int64))
+    ok = sorted(got) == plan["need"][rank] and all(torch.equal(got[a], rotated(a)) for a in got)
+    lo, hi = plan["ranges"][rank]
+    mine = pairs[plan["order"][lo:hi]]
+    part = ctx.spmspm(ca, cb, mine, dim, masks, keys) if len(mine) else None
+    if part is None:
+        part = np.zeros((2, L - 1, P.ring_degree), dtype=np.uint64)
+    t = torch.from_numpy(part.view(np.int64).copy())
+    reduce_partials(t, None)
+    full = host_mod(t.numpy().view(np.uint64), P.modulus_chain)
+    out_q.put((rank, full.tobytes(), len(mine), ok, len(owned),
+               sum(1 for a in got if plan["owner"][a] != rank)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_owned_alignments_exchanged_and_partials_combine(world):
+    """The product's shard planner + point-to-point exchange of owned
+    aligned operands + SUM all-reduce, world 2 and 3 over gloo."""
+    from paper_2604_11659_b200.dist import plan_shards
+    P, ctx, keys, ca, cb, pairs, dim, masks = _case()
+    want = ctx.spmspm(ca, cb, pairs, dim, masks, keys)
+    plan = plan_shards(pairs, dim, P.slots, world)
+    ctx_mp = mp.get_context("spawn")
+    q = ctx_mp.Queue()
+    port = _free_port()
+    procs = [ctx_mp.Process(target=_worker_owned, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert sum(g[2] for g in got) == len(pairs)
+    assert sum(g[4] for g in got) == len(plan["align"])      # each alignment computed once
+    assert any(g[5] for g in got)                              # something was actually exchanged
+    for rank, blob, _, ok, _, _ in got:
+        assert ok, rank
         arr = np.frombuffer(blob, dtype=np.uint64).reshape(want.shape)
         assert np.array_equal(arr, want), rank
 

@@ -407,3 +407,47 @@ def test_distributed_path_single_rank_nccl(pkg):
         assert res.ctxt.scale == full.ctxt.scale and res.ctxt.level == full.ctxt.level
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_owned_alignments_across_simulated_ranks(pkg, world):
+    """dist.py's multi-GPU plan on one GPU, ranks simulated in turn: each
+    rank's owned alignments computed once (hs_align_compute), handed to the
+    ranks that need them (hs_align_provide, no recomputation: the runner
+    reports 0 physical alignments), shard partials summed mod q == the
+    single-process result."""
+    import ctypes
+    import torch
+    from paper_2604_11659_b200 import device as D
+    from paper_2604_11659_b200 import dist as hdist
+    from paper_2604_11659_b200 import engine
+    from paper_2604_11659_b200._lib import check, lib
+    params, ctx, keys, a, b, ea, eb, full, counter, mc = product_runner_case(
+        pkg, 1024, 45, 2, 2024, 16, 0.5, 1 * 1_000_003 + 16 * 1_009)
+    L, n = params.levels, params.ring_degree
+    pairs = hdist._plan_pairs(ea, eb)
+    plan = hdist.plan_shards(pairs, 16, n // 2, world)
+    A = len(plan["align"])
+    aligned = D.empty((A, 2, L + 1, n))
+    for r in range(world):
+        mine = [x for x in range(A) if plan["owner"][x] == r]
+        srcs = (ctypes.c_int32 * len(mine))(*[plan["align"][x][0] for x in mine])
+        steps = (ctypes.c_uint32 * len(mine))(*[plan["align"][x][1] for x in mine])
+        outs = (ctypes.c_void_p * len(mine))(*[aligned[x].data_ptr() for x in mine])
+        check(lib().hs_align_compute(ctx.handle, D.ptr(ea.ctxt.data), D.ptr(eb.ctxt.data), srcs, steps,
+                                     len(mine), outs, D.stream()))
+    parts = []
+    for r in range(world):
+        ids = plan["need"][r]
+        srcs = (ctypes.c_int32 * len(ids))(*[plan["align"][x][0] for x in ids])
+        steps = (ctypes.c_uint32 * len(ids))(*[plan["align"][x][1] for x in ids])
+        ptrs = (ctypes.c_void_p * len(ids))(*[aligned[x].data_ptr() for x in ids])
+        check(lib().hs_align_provide(ctx.handle, srcs, steps, ptrs, len(ids)))
+        c = engine.OpCounter()
+        res = engine.run_pairs(ea, eb, ctx, keys, c, mc, pairs, shard=(r, world))
+        lib().hs_align_clear(ctx.handle)
+        assert c.physical_alignment == 0          # nothing recomputed
+        parts.append(res.ctxt.data.view(torch.int64).clone())
+    summed = torch.stack(parts).sum(0)
+    check(lib().hs_reduce_mod(ctx.handle, D.ptr(summed), 2, L - 1, D.stream()))
+    assert np.array_equal(D.to_host(summed.view(torch.uint64)), _arr(full.ctxt))

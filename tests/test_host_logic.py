@@ -88,3 +88,30 @@ def test_params_validation():
     with pytest.raises(ParameterError, match="duplicate"):
         CkksParams(64, (p.modulus_chain[0], p.modulus_chain[0]), 40, p.aux_prime)
     assert p.slots == 32 and p.levels == 2 and p.max_matrix_dim() == 5
+
+
+def test_shard_plan_owns_each_alignment_once_and_balances():
+    """dist.plan_shards on the bench workloads' real schedules (configs[1],
+    configs[2]): every distinct alignment rotation has exactly one owner,
+    owners carry at most ~1.1x (asserted: 1.3x) the ideal share, every rank's
+    needed set is covered, and the pair ranges match the runner's shard rule."""
+    import bench
+    from paper_2604_11659_b200 import dist, encmat, formats
+    from paper_2604_11659_b200.encmat import Layout, meta_and_values
+    for wl, dim, n in (("cfg2", 64, 1 << 14), ("cfg3", 128, 1 << 16)):
+        seed = bench.cell_seed(dim)
+        sp = bench.WORKLOADS[wl]["sparsity"]
+        a = formats.generate_random_sparse(dim, sp, (seed, 0))
+        b = formats.generate_random_sparse(dim, sp, (seed, 1))
+        ma, _ = meta_and_values(a, Layout.CSR)
+        mb, _ = meta_and_values(b, Layout.CSC)
+        pairs = encmat.pair_array(ma, mb)
+        for world in (2, 4, 8):
+            pl = dist.plan_shards(pairs, dim, n // 2, world)
+            A = len(pl["align"])
+            own = np.bincount(pl["owner"], minlength=world)
+            assert own.sum() == A and own.max() <= 1.3 * A / world, (wl, world, own.max(), A)
+            for r, (lo, hi) in enumerate(pl["ranges"]):
+                used = {int(pl["pair_align"][p]) for p in pl["order"][lo:hi] if pl["pair_align"][p] >= 0}
+                assert sorted(used) == pl["need"][r]
+            assert sum(hi - lo for lo, hi in pl["ranges"]) == len(pairs)
