@@ -977,6 +977,235 @@ __global__ void __launch_bounds__(RNG_T) pk_normal_write(ParArgs A, int digit) {
     }
 }
 
+// ============================================ digit-window uniform segments
+// The L+2 uniform segments of one digit (integers(0, q_m, n) for m = 0..L+1)
+// resolved WITHOUT a sequential chain of segment launches.  Rejections are
+// rare (p < q/2^64), so position r of the digit's stream (relative to the
+// digit start) lies in segment z = r / n ("zone") or z - 1:
+//  1. pk_uni_flags (all tiles, all keys): generate every draw of the window
+//     once, store two accept bitmaps -- under q_z (hi) and under q_{z-1}
+//     (lo) -- and per-tile popcounts;
+//  2. pk_uni_bounds (one warp per key): segment starts S_1..S_{L+2} in order
+//     (S_{m+1} = one past the n-th q_m-accept from S_m: hi bits up to the end
+//     of zone m, then lo bits of zone m+1), from tile counts + a few words;
+//  3. pk_uni_emit (all tiles): regenerate the draws; position r belongs to
+//     segment z if r >= S_z else z - 1; accepted draws are compacted with a
+//     decoupled look-back into the digit's flat [L+2][n] block of the a half
+//     (segment m's n values are exactly ranks m*n .. m*n+n-1).
+// If the cumulative rejections of a digit reach n (tiny rings) or the window
+// is too short, *err is set and the caller replays serially (exact either way).
+struct UniArgs {
+    unsigned* hib;          // [K][WU/32]
+    unsigned* lob;          // [K][WU/32]
+    u32* chi;               // [K][NTU]
+    u32* clo;               // [K][NTU]
+    u32* seg;               // [K][L+3] segment starts relative to the digit start
+    unsigned long long* flags;   // [K][NTU] look-back flags of pk_uni_emit
+    u32 WU, NTU;
+    int log_n;
+};
+
+__global__ void __launch_bounds__(RNG_T) pk_uni_flags(ParArgs A, UniArgs U) {
+    __shared__ U128 s_x;
+    __shared__ u32 s_h[RNG_W], s_l[RNG_W];
+    const int k = blockIdx.y, tile = blockIdx.x;
+    const u32 t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int L = A.L;
+    const KeyStream ks = A.streams[k];
+    const U128 inc{ks.inc_hi, ks.inc_lo};
+    U128 s = tile_state(A, ks, A.pos_in[k] + (u64)tile * RNG_CH, &s_x);
+    const U128 AT = A.jump->A[RNG_T], CT = mul128(A.jump->S[RNG_T], inc);
+    unsigned* hib = U.hib + (size_t)k * (U.WU / 32) + (size_t)tile * (RNG_CH / 32);
+    unsigned* lob = U.lob + (size_t)k * (U.WU / 32) + (size_t)tile * (RNG_CH / 32);
+    u32 ch = 0, cl = 0;
+#pragma unroll
+    for (int e = 0; e < RNG_E; e++) {
+        const u64 x = xsl_rr(s);
+        s = add128(mul128(s, AT), CT);
+        const u32 r = (u32)tile * RNG_CH + e * RNG_T + t;
+        const int z = (int)(r >> U.log_n);
+        bool hi = false, lo = false;
+        if (z <= L + 1) hi = x * A.pc[z].q >= A.thr[z];
+        if (z >= 1 && z <= L + 2) lo = x * A.pc[z - 1].q >= A.thr[z - 1];
+        const unsigned bh = __ballot_sync(0xffffffffu, hi), bl = __ballot_sync(0xffffffffu, lo);
+        if (lane == 0) {
+            hib[e * RNG_W + warp] = bh;
+            lob[e * RNG_W + warp] = bl;
+            ch += __popc(bh);
+            cl += __popc(bl);
+        }
+    }
+    if (lane == 0) {
+        s_h[warp] = ch;
+        s_l[warp] = cl;
+    }
+    __syncthreads();
+    if (t == 0) {
+        u32 a = 0, b = 0;
+        for (int w = 0; w < RNG_W; w++) {
+            a += s_h[w];
+            b += s_l[w];
+        }
+        U.chi[(size_t)k * U.NTU + tile] = a;
+        U.clo[(size_t)k * U.NTU + tile] = b;
+    }
+}
+
+// Set bits of bm in positions [a, b) (one warp; all lanes get the sum).
+HS_DEV u32 warp_count_words(const unsigned* bm, u32 a, u32 b, u32 lane) {
+    u32 c = 0;
+    if (a < b) {
+        for (u32 w = (a >> 5) + lane; w <= ((b - 1) >> 5); w += 32) {
+            unsigned x = bm[w];
+            const u32 base = w << 5;
+            if (base < a) x &= ~((1u << (a - base)) - 1u);
+            if (b - base < 32u) x &= (1u << (b - base)) - 1u;
+            c += __popc(x);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    return c;
+}
+
+// Set bits in [a, b): whole tiles from the per-tile counts, the rest by words.
+HS_DEV u32 warp_count_range(const unsigned* bm, const u32* tc, u32 a, u32 b, u32 lane) {
+    const u32 t0 = (a + RNG_CH - 1) / RNG_CH, t1 = b / RNG_CH;
+    if (t0 >= t1) return warp_count_words(bm, a, b, lane);
+    u32 c = 0;
+    for (u32 tt = t0 + lane; tt < t1; tt += 32) c += tc[tt];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    return c + warp_count_words(bm, a, t0 * RNG_CH, lane) + warp_count_words(bm, t1 * RNG_CH, b, lane);
+}
+
+// Position of the need-th (1-based) set bit at or after `from` (< limit), or
+// limit if there is none.  `from` is a word boundary.
+HS_DEV u32 warp_select(const unsigned* bm, u32 from, u32 need, u32 limit, u32 lane) {
+    for (u32 w0 = from >> 5; (w0 << 5) < limit; w0 += 32) {
+        const u32 w = w0 + lane;
+        const unsigned x = (w << 5) < limit ? bm[w] : 0u;
+        const u32 c = __popc(x);
+        u32 inc = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= (u32)o) inc += v;
+        }
+        const unsigned hit = __ballot_sync(0xffffffffu, inc >= need);
+        if (hit) {
+            const int f = __ffs(hit) - 1;
+            const u32 before = __shfl_sync(0xffffffffu, inc - c, f);
+            unsigned xf = __shfl_sync(0xffffffffu, x, f);
+            for (u32 r = 1; r < need - before; r++) xf &= xf - 1u;
+            return ((w0 + (u32)f) << 5) + (u32)(__ffs(xf) - 1);
+        }
+        need -= __shfl_sync(0xffffffffu, inc, 31);
+    }
+    return limit;
+}
+
+__global__ void __launch_bounds__(32) pk_uni_bounds(ParArgs A, UniArgs U) {
+    const int k = blockIdx.x;
+    const u32 lane = threadIdx.x;
+    const int L = A.L;
+    const u32 n = A.n;
+    const unsigned* hib = U.hib + (size_t)k * (U.WU / 32);
+    const unsigned* lob = U.lob + (size_t)k * (U.WU / 32);
+    const u32* chi = U.chi + (size_t)k * U.NTU;
+    u32* S = U.seg + (size_t)k * (L + 3);
+    u32 s = 0;
+    bool bad = false;
+    if (lane == 0) S[0] = 0;
+    for (int m = 0; m <= L + 1 && !bad; m++) {
+        const u32 z1 = (u32)(m + 1) * n;                       // end of zone m
+        const u32 a1 = warp_count_range(hib, chi, s, z1, lane);
+        u32 nx = z1;
+        if (a1 < n) {
+            const u32 p = warp_select(lob, z1, n - a1, U.WU, lane);
+            nx = p + 1;
+            // the next segment must start inside zone m+1 (fewer than n
+            // cumulative rejections) and inside the window
+            if (p >= U.WU || nx - z1 >= n) bad = true;
+        }
+        s = nx;
+        if (lane == 0) S[m + 1] = s;
+    }
+    if (lane == 0) {
+        if (bad) {
+            *A.err = 1;
+            A.pos_out[k] = A.pos_in[k];
+        } else {
+            A.pos_out[k] = A.pos_in[k] + s;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(RNG_T) pk_uni_emit(ParArgs A, UniArgs U, int digit, u32 seq) {
+    __shared__ U128 s_x;
+    __shared__ u32 cnt[RNG_E * RNG_W];
+    __shared__ u32 s_total, s_prefix;
+    __shared__ u32 s_seg[66];
+    const int k = blockIdx.y, tile = blockIdx.x;
+    const u32 t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const int L = A.L;
+    const u32 n = A.n;
+    unsigned long long* fl = U.flags + (size_t)k * U.NTU;
+    for (int m = t; m <= L + 2; m += RNG_T) s_seg[m] = U.seg[(size_t)k * (L + 3) + m];
+    __syncthreads();
+    const u32 end = s_seg[L + 2];
+    if ((u32)tile * RNG_CH >= end) {
+        if (t == 0) publish(fl + tile, seq, 0u);
+        return;
+    }
+    const KeyStream ks = A.streams[k];
+    const U128 inc{ks.inc_hi, ks.inc_lo};
+    U128 s = tile_state(A, ks, A.pos_in[k] + (u64)tile * RNG_CH, &s_x);
+    const U128 AT = A.jump->A[RNG_T], CT = mul128(A.jump->S[RNG_T], inc);
+    u64 val[RNG_E];
+    unsigned ball[RNG_E];
+#pragma unroll
+    for (int e = 0; e < RNG_E; e++) {
+        const u64 x = xsl_rr(s);
+        s = add128(mul128(s, AT), CT);
+        const u32 r = (u32)tile * RNG_CH + e * RNG_T + t;
+        const int z = (int)(r >> U.log_n);
+        const int sg = (z <= L + 1 && r >= s_seg[z]) ? z : z - 1;
+        const bool ok = r < end && sg >= 0 && sg <= L + 1;
+        const u64 q = A.pc[ok ? sg : 0].q;
+        val[e] = __umul64hi(x, q);
+        ball[e] = __ballot_sync(0xffffffffu, ok && x * q >= A.thr[ok ? sg : 0]);
+        if (lane == 0) cnt[e * RNG_W + warp] = __popc(ball[e]);
+    }
+    const u32 total = chunk_scan(cnt, &s_total);
+    if (t == 0) publish(fl + tile, seq, total);
+    if (warp == 0) {
+        const u32 p = look_back(fl, tile, seq);
+        if (lane == 0) s_prefix = p;
+    }
+    __syncthreads();
+    const u32 prefix = s_prefix;
+    const u32 lim = (u32)(L + 2) * n;
+    u64* dst = A.a_out[k] + (size_t)digit * (L + 2) * n;
+#pragma unroll
+    for (int e = 0; e < RNG_E; e++) {
+        if (!((ball[e] >> lane) & 1u)) continue;
+        const u32 idx = prefix + cnt[e * RNG_W + warp] + __popc(ball[e] & lt);
+        if (idx < lim) dst[idx] = val[e];
+    }
+}
+
+static u32 uni_window(u32 n, int L) {
+    const size_t w = (size_t)(L + 2) * n + std::max<size_t>(n / 2, 4096);
+    return (u32)((w + RNG_CH - 1) / RNG_CH * RNG_CH);
+}
+
+static size_t uni_scratch_bytes(int K, u32 n, int L) {
+    const size_t WU = uni_window(n, L), NTU = WU / RNG_CH;
+    return (size_t)K * (WU / 32 * 4 * 2 + NTU * 4 * 2 + (size_t)(L + 3) * 4 + NTU * 8) + 256;
+}
+
 size_t keygen_par_window(u32 n) {
     const size_t w = (size_t)n + n / 16 + 8192;
     return (w + RNG_CH - 1) / RNG_CH * RNG_CH;
@@ -994,8 +1223,8 @@ static size_t keygen_persist_scratch(int K, u32 n) {
     return (size_t)K * 64 * (NT + 1) * 8;
 }
 
-size_t keygen_par_scratch_bytes(int K, u32 n) {
-    return keygen_par_scratch_core(K, n) + keygen_persist_scratch(K, n) + 128;
+size_t keygen_par_scratch_bytes(int K, u32 n, int L) {
+    return keygen_par_scratch_core(K, n) + keygen_persist_scratch(K, n) + uni_scratch_bytes(K, n, L) + 256;
 }
 
 // Replays K key streams in lockstep.  Returns false (nothing guaranteed) if
@@ -1034,6 +1263,28 @@ void keygen_streams_parallel(const Dev& d, int K, const void* streams, u64* cons
     p += (size_t)K * nseg * NT * 8;
     unsigned long long* segpos = (unsigned long long*)p;    // [K][L+2] published segment starts
     cudaMemsetAsync(pflags, 0, (size_t)K * nseg * (NT + 1) * 8, st);
+    p += keygen_persist_scratch(K, d.n) - (size_t)K * nseg * NT * 8;
+    p = (char*)(((uintptr_t)p + 255) & ~(uintptr_t)255);
+    // digit-window uniform path (HS_KEYGEN_PERSIST=1: the persistent chain, A/B)
+    static const bool persist_only = getenv("HS_KEYGEN_PERSIST") != nullptr;
+    const bool uni = !persist_only && d.n >= 64;
+    UniArgs U{};
+    U.WU = uni_window(d.n, d.L);
+    U.NTU = U.WU / RNG_CH;
+    U.log_n = d.log_n;
+    U.hib = (unsigned*)p;
+    p += (size_t)K * (U.WU / 32) * 4;
+    U.lob = (unsigned*)p;
+    p += (size_t)K * (U.WU / 32) * 4;
+    U.chi = (u32*)p;
+    p += (size_t)K * U.NTU * 4;
+    U.clo = (u32*)p;
+    p += (size_t)K * U.NTU * 4;
+    U.seg = (u32*)p;
+    p += (size_t)K * (d.L + 3) * 4;
+    p = (char*)(((uintptr_t)p + 15) & ~(uintptr_t)15);
+    U.flags = (unsigned long long*)p;
+    if (uni) cudaMemsetAsync(U.flags, 0, (size_t)K * U.NTU * 8, st);
     u32 seq = 0;
     // keys per cooperative launch of the persistent uniform kernel (all its
     // CTAs must be co-resident); 0 = use one launch per segment
@@ -1047,6 +1298,7 @@ void keygen_streams_parallel(const Dev& d, int K, const void* streams, u64* cons
         coresident = (coop && !getenv("HS_KEYGEN_NO_PERSIST")) ? per * nsm : 0;
     }
     const int kgroup = coresident / NT;
+    u32 useq = 0;
     cudaMemsetAsync(pos[0], 0, (size_t)K * sizeof(u64), st);
     A.a_out = a_out;
     A.e_out = e_out;
@@ -1060,7 +1312,16 @@ void keygen_streams_parallel(const Dev& d, int K, const void* streams, u64* cons
     const size_t walk_smem = (size_t)5 * (W / 32) * sizeof(unsigned);
     cudaFuncSetAttribute(pk_normal_walk2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)walk_smem);
     for (int digit = 0; digit <= d.L; digit++) {
-        if (kgroup > 0) {
+        if (uni) {
+            A.pos_in = pos[cur];
+            A.pos_out = pos[cur ^ 1];
+            const dim3 gu(U.NTU, K);
+            pk_uni_flags<<<gu, RNG_T, 0, st>>>(A, U);
+            pk_uni_bounds<<<K, 32, 0, st>>>(A, U);
+            pk_uni_emit<<<gu, RNG_T, 0, st>>>(A, U, digit, ++useq);
+            note_launch(3);
+            cur ^= 1;
+        } else if (kgroup > 0) {
             A.pos_in = pos[cur];
             A.pos_out = pos[cur ^ 1];
             const u32 seq0 = seq + 1;
@@ -1364,7 +1625,7 @@ hs_status generate_galois_keys(hs_ctx* c, const std::vector<u32>& steps,
             HS_CUDA(cudaMemset(c->d_kg_err, 0, sizeof(int)));
         }
         // room for KG_LANES sub-chunk slices, each 256-byte aligned
-        HS_CUDA(cudaMallocAsync(&par_scratch, keygen_par_scratch_bytes(KB, c->n) + hs_ctx::KG_LANES * 512, st));
+        HS_CUDA(cudaMallocAsync(&par_scratch, keygen_par_scratch_bytes(KB, c->n, c->L) + hs_ctx::KG_LANES * 512, st));
     }
     for (size_t k0 = 0; k0 < steps.size(); k0 += KB) {
         const int K = (int)std::min<size_t>(KB, steps.size() - k0);
@@ -1401,7 +1662,7 @@ hs_status generate_galois_keys(hs_ctx* c, const std::vector<u32>& steps,
                 keygen_streams_parallel(c->dev, kc, d_streams + ka, d_aout + ka, e + (size_t)ka * (L + 1) * n,
                                         c->d_jump, c->d_zig, c->d_thr, (char*)par_scratch + soff,
                                         c->d_kg_err, sj);
-                soff += (keygen_par_scratch_bytes(kc, c->n) + 255) & ~(size_t)255;
+                soff += (keygen_par_scratch_bytes(kc, c->n, c->L) + 255) & ~(size_t)255;
                 keygen_assemble(c->dev, kc, d_keys + ka, e + (size_t)ka * (L + 1) * n, d_gal + ka, c->d_sk,
                                 c->d_kskf, skp + (size_t)ka * (L + 1) * n, sj);
                 HS_CUDA(cudaEventRecord(c->kg_event[j], sj));
@@ -1520,7 +1781,7 @@ hs_status hs_keygen_streams(hs_ctx* c, const uint64_t* states, int32_t nkeys, ui
         HS_CUDA(cudaMemset(c->d_kg_err, 0, sizeof(int)));
     }
     void* scratch = nullptr;
-    HS_CUDA(cudaMallocAsync(&scratch, keygen_par_scratch_bytes(nkeys, c->n), st));
+    HS_CUDA(cudaMallocAsync(&scratch, keygen_par_scratch_bytes(nkeys, c->n, c->L), st));
     keygen_streams_parallel(c->dev, nkeys, d_streams, d_aout, (long long*)e_out, c->d_jump, c->d_zig,
                             c->d_thr, scratch, c->d_kg_err, st);
     HS_CUDA(cudaStreamSynchronize(st));

@@ -111,7 +111,7 @@ void decrypt_combine(const Dev& d, int nl, const u64* ct, const u64* sk, u64* pt
 // ---- on-device Galois key generation (keygen.cu)
 void keygen_streams(const Dev& d, int K, const void* streams, u64* const* a_out, long long* e_out,
                     const void* jump, const void* zig, const u64* thr, cudaStream_t st);
-size_t keygen_par_scratch_bytes(int K, u32 n);
+size_t keygen_par_scratch_bytes(int K, u32 n, int L);
 void keygen_streams_parallel(const Dev& d, int K, const void* streams, u64* const* a_out,
                              long long* e_out, const void* jump, const void* zig, const u64* thr,
                              void* scratch, int* err, cudaStream_t st);
