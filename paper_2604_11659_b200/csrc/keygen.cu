@@ -31,6 +31,9 @@ constexpr int RNG_T = 512;              // threads per key CTA
 constexpr int RNG_E = 8;                // draws per thread per chunk (positions t + k*RNG_T)
 constexpr int RNG_CH = RNG_T * RNG_E;   // positions per chunk
 constexpr int RNG_W = RNG_T / 32;       // warps
+constexpr int UNI_E = 32;               // digit-window kernels: draws per thread per tile
+constexpr int UNI_TILE = RNG_T * UNI_E; // positions per tile (16384)
+constexpr int UNI_TW = UNI_TILE / 32;   // bitmap words per tile (512)
 
 struct U128 {
     u64 hi, lo;
@@ -65,6 +68,8 @@ struct RngJump {                          // for t = 0..RNG_CH: A_t = M^t, S_t =
     U128 S[RNG_CH + 1];
     U128 PA[64];                          // A_{2^j}
     U128 PS[64];                          // S_{2^j}
+    U128 TA[1024];                        // A_{t * UNI_TILE}: digit-window tiles (t < 1024)
+    U128 TS[1024];                        // S_{t * UNI_TILE}
 };
 
 struct KeyStream {
@@ -982,72 +987,103 @@ __global__ void __launch_bounds__(RNG_T) pk_normal_write(ParArgs A, int digit) {
 // resolved WITHOUT a sequential chain of segment launches.  Rejections are
 // rare (p < q/2^64), so position r of the digit's stream (relative to the
 // digit start) lies in segment z = r / n ("zone") or z - 1:
+//  0. pk_uni_start (one warp per key): PCG64 state at the digit start (binary
+//     composition of power-of-two jumps); every tile then jumps from it with
+//     one affine map from a table (TA/TS, tiles of UNI_TILE draws);
 //  1. pk_uni_flags (all tiles, all keys): generate every draw of the window
 //     once, store two accept bitmaps -- under q_z (hi) and under q_{z-1}
 //     (lo) -- and per-tile popcounts;
 //  2. pk_uni_bounds (one warp per key): segment starts S_1..S_{L+2} in order
 //     (S_{m+1} = one past the n-th q_m-accept from S_m: hi bits up to the end
 //     of zone m, then lo bits of zone m+1), from tile counts + a few words;
-//  3. pk_uni_emit (all tiles): regenerate the draws; position r belongs to
-//     segment z if r >= S_z else z - 1; accepted draws are compacted with a
-//     decoupled look-back into the digit's flat [L+2][n] block of the a half
-//     (segment m's n values are exactly ranks m*n .. m*n+n-1).
+//  3. pk_uni_emit (all tiles): effective accept bits (hi if r >= S_z, else lo)
+//     from the bitmaps, tile totals chained by decoupled look-back, then the
+//     draws regenerated once more for their values; accepted draws land at
+//     their rank in the digit's flat [L+2][n] block of the a half (segment m's
+//     n values are exactly ranks m*n .. m*n+n-1).
 // If the cumulative rejections of a digit reach n (tiny rings) or the window
 // is too short, *err is set and the caller replays serially (exact either way).
 struct UniArgs {
     unsigned* hib;          // [K][WU/32]
     unsigned* lob;          // [K][WU/32]
     u32* chi;               // [K][NTU]
-    u32* clo;               // [K][NTU]
     u32* seg;               // [K][L+3] segment starts relative to the digit start
+    U128* s0;               // [K] PCG64 state at the digit start
     unsigned long long* flags;   // [K][NTU] look-back flags of pk_uni_emit
     u32 WU, NTU;
     int log_n;
 };
 
+__global__ void __launch_bounds__(32) pk_uni_start(ParArgs A, UniArgs U) {
+    const int k = blockIdx.x;
+    const u32 l = threadIdx.x;
+    const KeyStream ks = A.streams[k];
+    const U128 inc{ks.inc_hi, ks.inc_lo};
+    const u64 P = A.pos_in[k];
+    U128 Am{0, 1}, Bm{0, 0};
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        const u32 j = l + 32u * h;
+        if ((P >> j) & 1ull) {
+            const U128 Aj = A.jump->PA[j], Bj = mul128(A.jump->PS[j], inc);
+            Bm = add128(mul128(Aj, Bm), Bj);
+            Am = mul128(Aj, Am);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        U128 Ao, Bo;
+        Ao.hi = __shfl_xor_sync(0xffffffffu, Am.hi, o);
+        Ao.lo = __shfl_xor_sync(0xffffffffu, Am.lo, o);
+        Bo.hi = __shfl_xor_sync(0xffffffffu, Bm.hi, o);
+        Bo.lo = __shfl_xor_sync(0xffffffffu, Bm.lo, o);
+        Bm = add128(mul128(Ao, Bm), Bo);
+        Am = mul128(Ao, Am);
+    }
+    if (l == 0) U.s0[k] = add128(mul128(Am, U128{ks.state_hi, ks.state_lo}), Bm);
+}
+
+// State whose output is the draw at window position tile*UNI_TILE + t.
+HS_DEV U128 uni_thread_state(const ParArgs& A, const UniArgs& U, int k, int tile, const U128& inc) {
+    const U128 s0 = U.s0[k];
+    const U128 T = add128(mul128(A.jump->TA[tile], s0), mul128(A.jump->TS[tile], inc));
+    return add128(mul128(A.jump->A[threadIdx.x + 1], T), mul128(A.jump->S[threadIdx.x + 1], inc));
+}
+
 __global__ void __launch_bounds__(RNG_T) pk_uni_flags(ParArgs A, UniArgs U) {
-    __shared__ U128 s_x;
-    __shared__ u32 s_h[RNG_W], s_l[RNG_W];
+    __shared__ u32 s_h[RNG_W];
     const int k = blockIdx.y, tile = blockIdx.x;
     const u32 t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int L = A.L;
     const KeyStream ks = A.streams[k];
     const U128 inc{ks.inc_hi, ks.inc_lo};
-    U128 s = tile_state(A, ks, A.pos_in[k] + (u64)tile * RNG_CH, &s_x);
+    U128 s = uni_thread_state(A, U, k, tile, inc);
     const U128 AT = A.jump->A[RNG_T], CT = mul128(A.jump->S[RNG_T], inc);
-    unsigned* hib = U.hib + (size_t)k * (U.WU / 32) + (size_t)tile * (RNG_CH / 32);
-    unsigned* lob = U.lob + (size_t)k * (U.WU / 32) + (size_t)tile * (RNG_CH / 32);
-    u32 ch = 0, cl = 0;
-#pragma unroll
-    for (int e = 0; e < RNG_E; e++) {
+    unsigned* hib = U.hib + (size_t)k * (U.WU / 32) + (size_t)tile * UNI_TW;
+    unsigned* lob = U.lob + (size_t)k * (U.WU / 32) + (size_t)tile * UNI_TW;
+    u32 ch = 0;
+#pragma unroll 4
+    for (int e = 0; e < UNI_E; e++) {
         const u64 x = xsl_rr(s);
         s = add128(mul128(s, AT), CT);
-        const u32 r = (u32)tile * RNG_CH + e * RNG_T + t;
+        const u32 r = (u32)tile * UNI_TILE + e * RNG_T + t;
         const int z = (int)(r >> U.log_n);
         bool hi = false, lo = false;
-        if (z <= L + 1) hi = x * A.pc[z].q >= A.thr[z];
-        if (z >= 1 && z <= L + 2) lo = x * A.pc[z - 1].q >= A.thr[z - 1];
+        if (z <= L + 1) hi = x * __ldg(&A.pc[z].q) >= __ldg(A.thr + z);
+        if (z >= 1 && z <= L + 2) lo = x * __ldg(&A.pc[z - 1].q) >= __ldg(A.thr + z - 1);
         const unsigned bh = __ballot_sync(0xffffffffu, hi), bl = __ballot_sync(0xffffffffu, lo);
         if (lane == 0) {
             hib[e * RNG_W + warp] = bh;
             lob[e * RNG_W + warp] = bl;
             ch += __popc(bh);
-            cl += __popc(bl);
         }
     }
-    if (lane == 0) {
-        s_h[warp] = ch;
-        s_l[warp] = cl;
-    }
+    if (lane == 0) s_h[warp] = ch;
     __syncthreads();
     if (t == 0) {
-        u32 a = 0, b = 0;
-        for (int w = 0; w < RNG_W; w++) {
-            a += s_h[w];
-            b += s_l[w];
-        }
+        u32 a = 0;
+        for (int w = 0; w < RNG_W; w++) a += s_h[w];
         U.chi[(size_t)k * U.NTU + tile] = a;
-        U.clo[(size_t)k * U.NTU + tile] = b;
     }
 }
 
@@ -1070,13 +1106,13 @@ HS_DEV u32 warp_count_words(const unsigned* bm, u32 a, u32 b, u32 lane) {
 
 // Set bits in [a, b): whole tiles from the per-tile counts, the rest by words.
 HS_DEV u32 warp_count_range(const unsigned* bm, const u32* tc, u32 a, u32 b, u32 lane) {
-    const u32 t0 = (a + RNG_CH - 1) / RNG_CH, t1 = b / RNG_CH;
+    const u32 t0 = (a + UNI_TILE - 1) / UNI_TILE, t1 = b / UNI_TILE;
     if (t0 >= t1) return warp_count_words(bm, a, b, lane);
     u32 c = 0;
     for (u32 tt = t0 + lane; tt < t1; tt += 32) c += tc[tt];
 #pragma unroll
     for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    return c + warp_count_words(bm, a, t0 * RNG_CH, lane) + warp_count_words(bm, t1 * RNG_CH, b, lane);
+    return c + warp_count_words(bm, a, t0 * UNI_TILE, lane) + warp_count_words(bm, t1 * UNI_TILE, b, lane);
 }
 
 // Position of the need-th (1-based) set bit at or after `from` (< limit), or
@@ -1142,9 +1178,10 @@ __global__ void __launch_bounds__(32) pk_uni_bounds(ParArgs A, UniArgs U) {
 }
 
 __global__ void __launch_bounds__(RNG_T) pk_uni_emit(ParArgs A, UniArgs U, int digit, u32 seq) {
-    __shared__ U128 s_x;
-    __shared__ u32 cnt[RNG_E * RNG_W];
-    __shared__ u32 s_total, s_prefix;
+    __shared__ unsigned s_eff[UNI_TW];
+    __shared__ u32 s_pre[UNI_TW];
+    __shared__ u32 s_wsum[RNG_W];
+    __shared__ u32 s_prefix;
     __shared__ u32 s_seg[66];
     const int k = blockIdx.y, tile = blockIdx.x;
     const u32 t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -1155,31 +1192,44 @@ __global__ void __launch_bounds__(RNG_T) pk_uni_emit(ParArgs A, UniArgs U, int d
     for (int m = t; m <= L + 2; m += RNG_T) s_seg[m] = U.seg[(size_t)k * (L + 3) + m];
     __syncthreads();
     const u32 end = s_seg[L + 2];
-    if ((u32)tile * RNG_CH >= end) {
+    const u32 base = (u32)tile * UNI_TILE;
+    if (base >= end) {
         if (t == 0) publish(fl + tile, seq, 0u);
         return;
     }
-    const KeyStream ks = A.streams[k];
-    const U128 inc{ks.inc_hi, ks.inc_lo};
-    U128 s = tile_state(A, ks, A.pos_in[k] + (u64)tile * RNG_CH, &s_x);
-    const U128 AT = A.jump->A[RNG_T], CT = mul128(A.jump->S[RNG_T], inc);
-    u64 val[RNG_E];
-    unsigned ball[RNG_E];
+    // ---- effective accept bits of this tile (one word per thread: UNI_TW == RNG_T)
+    {
+        const u32 w = t;
+        const u32 p0 = base + 32u * w;                         // first position of the word
+        const int z = (int)(p0 >> U.log_n);                    // one zone per word (n >= 64)
+        const size_t gw = (size_t)k * (U.WU / 32) + (size_t)tile * UNI_TW + w;
+        const unsigned hi = U.hib[gw], lo = U.lob[gw];
+        const u32 sz = z <= L + 1 ? s_seg[z] : end;            // positions >= sz are in segment z
+        unsigned m_hi;                                          // word bits at positions >= sz
+        if (sz <= p0) m_hi = 0xffffffffu;
+        else if (sz >= p0 + 32u) m_hi = 0u;
+        else m_hi = ~((1u << (sz - p0)) - 1u);
+        unsigned e = (z <= L + 1 ? (hi & m_hi) : 0u) | (z >= 1 ? (lo & ~m_hi) : 0u);
+        if (p0 >= end) e = 0u;
+        else if (end - p0 < 32u) e &= (1u << (end - p0)) - 1u;
+        s_eff[w] = e;
+        // exclusive scan of word popcounts over the tile
+        const u32 c = __popc(e);
+        u32 inc = c;
 #pragma unroll
-    for (int e = 0; e < RNG_E; e++) {
-        const u64 x = xsl_rr(s);
-        s = add128(mul128(s, AT), CT);
-        const u32 r = (u32)tile * RNG_CH + e * RNG_T + t;
-        const int z = (int)(r >> U.log_n);
-        const int sg = (z <= L + 1 && r >= s_seg[z]) ? z : z - 1;
-        const bool ok = r < end && sg >= 0 && sg <= L + 1;
-        const u64 q = A.pc[ok ? sg : 0].q;
-        val[e] = __umul64hi(x, q);
-        ball[e] = __ballot_sync(0xffffffffu, ok && x * q >= A.thr[ok ? sg : 0]);
-        if (lane == 0) cnt[e * RNG_W + warp] = __popc(ball[e]);
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= (u32)o) inc += v;
+        }
+        if (lane == 31) s_wsum[warp] = inc;
+        __syncthreads();
+        u32 before = 0;
+        for (u32 j = 0; j < warp; j++) before += s_wsum[j];
+        s_pre[w] = before + inc - c;
+        if (t == RNG_T - 1) {
+            publish(fl + tile, seq, before + inc);
+        }
     }
-    const u32 total = chunk_scan(cnt, &s_total);
-    if (t == 0) publish(fl + tile, seq, total);
     if (warp == 0) {
         const u32 p = look_back(fl, tile, seq);
         if (lane == 0) s_prefix = p;
@@ -1188,22 +1238,33 @@ __global__ void __launch_bounds__(RNG_T) pk_uni_emit(ParArgs A, UniArgs U, int d
     const u32 prefix = s_prefix;
     const u32 lim = (u32)(L + 2) * n;
     u64* dst = A.a_out[k] + (size_t)digit * (L + 2) * n;
-#pragma unroll
-    for (int e = 0; e < RNG_E; e++) {
-        if (!((ball[e] >> lane) & 1u)) continue;
-        const u32 idx = prefix + cnt[e * RNG_W + warp] + __popc(ball[e] & lt);
-        if (idx < lim) dst[idx] = val[e];
+    const KeyStream ks = A.streams[k];
+    const U128 inc{ks.inc_hi, ks.inc_lo};
+    U128 s = uni_thread_state(A, U, k, tile, inc);
+    const U128 AT = A.jump->A[RNG_T], CT = mul128(A.jump->S[RNG_T], inc);
+#pragma unroll 4
+    for (int e = 0; e < UNI_E; e++) {
+        const u64 x = xsl_rr(s);
+        s = add128(mul128(s, AT), CT);
+        const u32 w = e * RNG_W + warp;
+        const unsigned eb = s_eff[w];
+        if (!((eb >> lane) & 1u)) continue;
+        const u32 r = base + e * RNG_T + t;
+        const int z = (int)(r >> U.log_n);
+        const int sg = (z <= L + 1 && r >= s_seg[z]) ? z : z - 1;
+        const u32 idx = prefix + s_pre[w] + __popc(eb & lt);
+        if (idx < lim) dst[idx] = __umul64hi(x, __ldg(&A.pc[sg].q));
     }
 }
 
 static u32 uni_window(u32 n, int L) {
     const size_t w = (size_t)(L + 2) * n + std::max<size_t>(n / 2, 4096);
-    return (u32)((w + RNG_CH - 1) / RNG_CH * RNG_CH);
+    return (u32)((w + UNI_TILE - 1) / UNI_TILE * UNI_TILE);      // <= 1024 tiles (L <= 62, n <= 2^17)
 }
 
 static size_t uni_scratch_bytes(int K, u32 n, int L) {
-    const size_t WU = uni_window(n, L), NTU = WU / RNG_CH;
-    return (size_t)K * (WU / 32 * 4 * 2 + NTU * 4 * 2 + (size_t)(L + 3) * 4 + NTU * 8) + 256;
+    const size_t WU = uni_window(n, L), NTU = WU / UNI_TILE;
+    return (size_t)K * (WU / 32 * 4 * 2 + NTU * 4 + (size_t)(L + 3) * 4 + 16 + NTU * 8) + 512;
 }
 
 size_t keygen_par_window(u32 n) {
@@ -1267,10 +1328,10 @@ void keygen_streams_parallel(const Dev& d, int K, const void* streams, u64* cons
     p = (char*)(((uintptr_t)p + 255) & ~(uintptr_t)255);
     // digit-window uniform path (HS_KEYGEN_PERSIST=1: the persistent chain, A/B)
     static const bool persist_only = getenv("HS_KEYGEN_PERSIST") != nullptr;
-    const bool uni = !persist_only && d.n >= 64;
+    const bool uni = !persist_only && d.n >= 64 && uni_window(d.n, d.L) / UNI_TILE <= 1024;
     UniArgs U{};
     U.WU = uni_window(d.n, d.L);
-    U.NTU = U.WU / RNG_CH;
+    U.NTU = U.WU / UNI_TILE;
     U.log_n = d.log_n;
     U.hib = (unsigned*)p;
     p += (size_t)K * (U.WU / 32) * 4;
@@ -1278,11 +1339,11 @@ void keygen_streams_parallel(const Dev& d, int K, const void* streams, u64* cons
     p += (size_t)K * (U.WU / 32) * 4;
     U.chi = (u32*)p;
     p += (size_t)K * U.NTU * 4;
-    U.clo = (u32*)p;
-    p += (size_t)K * U.NTU * 4;
     U.seg = (u32*)p;
     p += (size_t)K * (d.L + 3) * 4;
     p = (char*)(((uintptr_t)p + 15) & ~(uintptr_t)15);
+    U.s0 = (U128*)p;
+    p += (size_t)K * sizeof(U128);
     U.flags = (unsigned long long*)p;
     if (uni) cudaMemsetAsync(U.flags, 0, (size_t)K * U.NTU * 8, st);
     u32 seq = 0;
@@ -1316,10 +1377,11 @@ void keygen_streams_parallel(const Dev& d, int K, const void* streams, u64* cons
             A.pos_in = pos[cur];
             A.pos_out = pos[cur ^ 1];
             const dim3 gu(U.NTU, K);
+            pk_uni_start<<<K, 32, 0, st>>>(A, U);
             pk_uni_flags<<<gu, RNG_T, 0, st>>>(A, U);
             pk_uni_bounds<<<K, 32, 0, st>>>(A, U);
             pk_uni_emit<<<gu, RNG_T, 0, st>>>(A, U, digit, ++useq);
-            note_launch(3);
+            note_launch(4);
             cur ^= 1;
         } else if (kgroup > 0) {
             A.pos_in = pos[cur];
@@ -1530,6 +1592,18 @@ hs_status ensure_keygen_tables(hs_ctx* c) {
             J->PS[j] = U128{(u64)(ps >> 64), (u64)ps};
             ps = ps + pa * ps;
             pa = pa * pa;
+        }
+    }
+    {   // digit-window tile jumps: (TA, TS)_{t+1} = (TA_t A_U, TS_t + TA_t S_U), U = UNI_TILE = 2^14
+        static_assert(UNI_TILE == 1 << 14, "UNI_TILE is a power of two");
+        const u128h au = ((u128h)J->PA[14].hi << 64) | J->PA[14].lo;
+        const u128h su = ((u128h)J->PS[14].hi << 64) | J->PS[14].lo;
+        u128h ta = 1, ts = 0;
+        for (int t = 0; t < 1024; t++) {
+            J->TA[t] = U128{(u64)(ta >> 64), (u64)ta};
+            J->TS[t] = U128{(u64)(ts >> 64), (u64)ts};
+            ts = ts + ta * su;
+            ta = ta * au;
         }
     }
     std::vector<u64> thr(L + 2);
