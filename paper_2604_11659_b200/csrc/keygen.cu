@@ -34,6 +34,7 @@ constexpr int RNG_W = RNG_T / 32;       // warps
 constexpr int UNI_E = 32;               // digit-window kernels: draws per thread per tile
 constexpr int UNI_TILE = RNG_T * UNI_E; // positions per tile (16384)
 constexpr int UNI_TW = UNI_TILE / 32;   // bitmap words per tile (512)
+static_assert(UNI_E == 32, "pk_uni_flags keeps draw e's bitmap words in lane e");
 
 struct U128 {
     u64 hi, lo;
@@ -1050,34 +1051,59 @@ HS_DEV U128 uni_thread_state(const ParArgs& A, const UniArgs& U, int k, int tile
     return add128(mul128(A.jump->A[threadIdx.x + 1], T), mul128(A.jump->S[threadIdx.x + 1], inc));
 }
 
+// ZU: every tile lies inside one zone (n >= UNI_TILE): the two candidate
+// moduli and thresholds are CTA constants; otherwise they are looked up per
+// position from shared memory.
+template <bool ZU>
 __global__ void __launch_bounds__(RNG_T) pk_uni_flags(ParArgs A, UniArgs U) {
     __shared__ u32 s_h[RNG_W];
+    __shared__ u64 s_q[66], s_t[66];
     const int k = blockIdx.y, tile = blockIdx.x;
     const u32 t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int L = A.L;
+    if (!ZU) {
+        for (int m = t; m <= L + 1; m += RNG_T) {
+            s_q[m] = A.pc[m].q;
+            s_t[m] = A.thr[m];
+        }
+        __syncthreads();
+    }
     const KeyStream ks = A.streams[k];
     const U128 inc{ks.inc_hi, ks.inc_lo};
     U128 s = uni_thread_state(A, U, k, tile, inc);
     const U128 AT = A.jump->A[RNG_T], CT = mul128(A.jump->S[RNG_T], inc);
-    unsigned* hib = U.hib + (size_t)k * (U.WU / 32) + (size_t)tile * UNI_TW;
-    unsigned* lob = U.lob + (size_t)k * (U.WU / 32) + (size_t)tile * UNI_TW;
+    const int zt = (int)(((u32)tile * UNI_TILE) >> U.log_n);      // the tile's zone (ZU)
+    const bool hv = zt <= L + 1, lv = zt >= 1 && zt <= L + 2;
+    const u64 qh = hv ? __ldg(&A.pc[zt].q) : 0ull, th = hv ? __ldg(A.thr + zt) : 0ull;
+    const u64 ql = lv ? __ldg(&A.pc[zt - 1].q) : 0ull, tl = lv ? __ldg(A.thr + zt - 1) : 0ull;
+    unsigned myh = 0u, myl = 0u;                                 // lane e keeps the words of draw e
     u32 ch = 0;
 #pragma unroll 4
     for (int e = 0; e < UNI_E; e++) {
         const u64 x = xsl_rr(s);
         s = add128(mul128(s, AT), CT);
-        const u32 r = (u32)tile * UNI_TILE + e * RNG_T + t;
-        const int z = (int)(r >> U.log_n);
-        bool hi = false, lo = false;
-        if (z <= L + 1) hi = x * __ldg(&A.pc[z].q) >= __ldg(A.thr + z);
-        if (z >= 1 && z <= L + 2) lo = x * __ldg(&A.pc[z - 1].q) >= __ldg(A.thr + z - 1);
+        bool hi, lo;
+        if (ZU) {
+            hi = hv && x * qh >= th;
+            lo = lv && x * ql >= tl;
+        } else {
+            const u32 r = (u32)tile * UNI_TILE + e * RNG_T + t;
+            const int z = (int)(r >> U.log_n);
+            hi = z <= L + 1 && x * s_q[z] >= s_t[z];
+            lo = z >= 1 && z <= L + 2 && x * s_q[z - 1] >= s_t[z - 1];
+        }
         const unsigned bh = __ballot_sync(0xffffffffu, hi), bl = __ballot_sync(0xffffffffu, lo);
-        if (lane == 0) {
-            hib[e * RNG_W + warp] = bh;
-            lob[e * RNG_W + warp] = bl;
-            ch += __popc(bh);
+        ch += __popc(bh);
+        if (lane == (u32)e) {
+            myh = bh;
+            myl = bl;
         }
     }
+    // word of draw e (positions e*RNG_T + warp*32 ...) = tile word e*RNG_W + warp
+    unsigned* hib = U.hib + (size_t)k * (U.WU / 32) + (size_t)tile * UNI_TW;
+    unsigned* lob = U.lob + (size_t)k * (U.WU / 32) + (size_t)tile * UNI_TW;
+    hib[lane * RNG_W + warp] = myh;
+    lob[lane * RNG_W + warp] = myl;
     if (lane == 0) s_h[warp] = ch;
     __syncthreads();
     if (t == 0) {
@@ -1141,7 +1167,17 @@ HS_DEV u32 warp_select(const unsigned* bm, u32 from, u32 need, u32 limit, u32 la
     return limit;
 }
 
+// Segment starts of one key's digit window.  Fast path (n >= UNI_TILE, so
+// tiles align with zones): zone totals of the hi bits come from the per-tile
+// counts, and the first 32 words of every zone's hi and lo bitmaps are
+// prefetched into shared memory in one parallel pass, so the serial chain
+// over the L+2 segments only touches shared memory (segment starts lie within
+// 1024 positions of their zone start unless a digit has > 1024 rejections,
+// which falls back to the global-memory walk).
+constexpr int UB_W = 32;                      // prefetched words per zone
 __global__ void __launch_bounds__(32) pk_uni_bounds(ParArgs A, UniArgs U) {
+    __shared__ unsigned sh[66][UB_W], sl[66][UB_W];
+    __shared__ u32 ztot[66];
     const int k = blockIdx.x;
     const u32 lane = threadIdx.x;
     const int L = A.L;
@@ -1150,15 +1186,70 @@ __global__ void __launch_bounds__(32) pk_uni_bounds(ParArgs A, UniArgs U) {
     const unsigned* lob = U.lob + (size_t)k * (U.WU / 32);
     const u32* chi = U.chi + (size_t)k * U.NTU;
     u32* S = U.seg + (size_t)k * (L + 3);
+    const bool fast = n >= (u32)UNI_TILE;
+    if (fast) {
+        const u32 tpz = n / UNI_TILE;                          // tiles per zone
+        for (int m = 0; m <= L + 2; m++) {
+            const u32 w0 = (u32)m * (n / 32);
+            const bool in = (w0 + lane) * 32u < U.WU;
+            sh[m][lane] = in ? hib[w0 + lane] : 0u;
+            sl[m][lane] = in ? lob[w0 + lane] : 0u;
+            u32 c = 0;
+            for (u32 j = lane; j < tpz; j += 32) {
+                const u32 tt = (u32)m * tpz + j;
+                c += tt < U.NTU ? chi[tt] : 0u;
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+            if (lane == 0) ztot[m] = c;
+        }
+        __syncwarp();
+    }
     u32 s = 0;
     bool bad = false;
     if (lane == 0) S[0] = 0;
     for (int m = 0; m <= L + 1 && !bad; m++) {
-        const u32 z1 = (u32)(m + 1) * n;                       // end of zone m
-        const u32 a1 = warp_count_range(hib, chi, s, z1, lane);
+        const u32 z0 = (u32)m * n, z1 = z0 + n;                // zone m = [z0, z1)
+        u32 a1;
+        if (fast && s - z0 < UB_W * 32u) {
+            // hi bits in [s, z1) = zone total - hi bits in [z0, s)
+            const u32 off = s - z0;
+            unsigned x = sh[m][lane];
+            const u32 b0 = lane * 32u;
+            if (off <= b0) x = 0u;
+            else if (off - b0 < 32u) x &= (1u << (off - b0)) - 1u;
+            u32 c = __popc(x);
+#pragma unroll
+            for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+            a1 = ztot[m] - c;
+        } else {
+            a1 = warp_count_range(hib, chi, s, z1, lane);
+        }
         u32 nx = z1;
         if (a1 < n) {
-            const u32 p = warp_select(lob, z1, n - a1, U.WU, lane);
+            const u32 need = n - a1;
+            u32 p = U.WU;
+            bool found = false;
+            if (fast && m + 1 <= L + 2) {
+                const unsigned x = sl[m + 1][lane];
+                const u32 c = __popc(x);
+                u32 inc = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const u32 v = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= (u32)o) inc += v;
+                }
+                const unsigned hit = __ballot_sync(0xffffffffu, inc >= need);
+                if (hit) {
+                    const int f = __ffs(hit) - 1;
+                    const u32 before = __shfl_sync(0xffffffffu, inc - c, f);
+                    unsigned xf = __shfl_sync(0xffffffffu, x, f);
+                    for (u32 r = 1; r < need - before; r++) xf &= xf - 1u;
+                    p = z1 + (u32)f * 32u + (u32)(__ffs(xf) - 1);
+                    found = true;
+                }
+            }
+            if (!found) p = warp_select(lob, z1, need, U.WU, lane);
             nx = p + 1;
             // the next segment must start inside zone m+1 (fewer than n
             // cumulative rejections) and inside the window
@@ -1242,6 +1333,11 @@ __global__ void __launch_bounds__(RNG_T) pk_uni_emit(ParArgs A, UniArgs U, int d
     const U128 inc{ks.inc_hi, ks.inc_lo};
     U128 s = uni_thread_state(A, U, k, tile, inc);
     const U128 AT = A.jump->A[RNG_T], CT = mul128(A.jump->S[RNG_T], inc);
+    // candidate moduli of the tile's zone (exact when the tile lies in one zone)
+    const int zt = (int)(base >> U.log_n);
+    const bool one_zone = ((base + UNI_TILE - 1) >> U.log_n) == (u32)zt;
+    const u64 qh = zt <= L + 1 ? __ldg(&A.pc[zt].q) : 0ull, ql = zt >= 1 ? __ldg(&A.pc[zt - 1].q) : 0ull;
+    const u32 szt = zt <= L + 1 ? s_seg[zt] : end;
 #pragma unroll 4
     for (int e = 0; e < UNI_E; e++) {
         const u64 x = xsl_rr(s);
@@ -1250,10 +1346,15 @@ __global__ void __launch_bounds__(RNG_T) pk_uni_emit(ParArgs A, UniArgs U, int d
         const unsigned eb = s_eff[w];
         if (!((eb >> lane) & 1u)) continue;
         const u32 r = base + e * RNG_T + t;
-        const int z = (int)(r >> U.log_n);
-        const int sg = (z <= L + 1 && r >= s_seg[z]) ? z : z - 1;
+        u64 q;
+        if (one_zone) {
+            q = r >= szt ? qh : ql;
+        } else {
+            const int z = (int)(r >> U.log_n);
+            q = __ldg(&A.pc[(z <= L + 1 && r >= s_seg[z]) ? z : z - 1].q);
+        }
         const u32 idx = prefix + s_pre[w] + __popc(eb & lt);
-        if (idx < lim) dst[idx] = __umul64hi(x, __ldg(&A.pc[sg].q));
+        if (idx < lim) dst[idx] = __umul64hi(x, q);
     }
 }
 
@@ -1378,7 +1479,8 @@ void keygen_streams_parallel(const Dev& d, int K, const void* streams, u64* cons
             A.pos_out = pos[cur ^ 1];
             const dim3 gu(U.NTU, K);
             pk_uni_start<<<K, 32, 0, st>>>(A, U);
-            pk_uni_flags<<<gu, RNG_T, 0, st>>>(A, U);
+            if (d.n >= (u32)UNI_TILE) pk_uni_flags<true><<<gu, RNG_T, 0, st>>>(A, U);
+            else pk_uni_flags<false><<<gu, RNG_T, 0, st>>>(A, U);
             pk_uni_bounds<<<K, 32, 0, st>>>(A, U);
             pk_uni_emit<<<gu, RNG_T, 0, st>>>(A, U, digit, ++useq);
             note_launch(4);
