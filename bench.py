@@ -73,6 +73,17 @@ WORKLOADS = {
                   lazy_keys=True, batch_gb=16, tiled=True,
                   desc="configs[3] scale: N=2^16, L=24, 256x256 @99% as 2x2 tiles of 128x128 "
                        "ciphertexts (multi-ciphertext tiling)"),
+    "cfg4": dict(ring_degree=1 << 16, scale_bits=50, levels=24, seed=2024, dim=256, sparsity=0.9,
+                 lazy_keys=True, batch_gb=16, tiled=True,
+                 desc="configs[3]: N=2^16, L=24, 256x256 @90% as 2x2 tiles of 128x128 ciphertexts"),
+    # configs[4]: 512x512 needs 262,144 slots > 65,536 at N=2^17 -> 2x2 tiles of 256x256;
+    # keys 2.8 GB each (36 digits x 37 moduli x 1 MiB x 2), generated on device
+    "cfg5_99": dict(ring_degree=1 << 17, scale_bits=50, levels=35, seed=2024, dim=512, sparsity=0.99,
+                    lazy_keys=True, batch_gb=24, tiled=True,
+                    desc="configs[4] at 99% sparsity: N=2^17, L=35, 512x512 as 2x2 tiles of 256x256"),
+    "cfg5_98": dict(ring_degree=1 << 17, scale_bits=50, levels=35, seed=2024, dim=512, sparsity=0.98,
+                    lazy_keys=True, batch_gb=24, tiled=True,
+                    desc="configs[4] at 98% sparsity: N=2^17, L=35, 512x512 as 2x2 tiles of 256x256"),
 }
 
 

@@ -1188,21 +1188,20 @@ __global__ void __launch_bounds__(32) pk_uni_bounds(ParArgs A, UniArgs U) {
     u32* S = U.seg + (size_t)k * (L + 3);
     const bool fast = n >= (u32)UNI_TILE;
     if (fast) {
+        // all loads independent: unrolled so many are in flight at once
         const u32 tpz = n / UNI_TILE;                          // tiles per zone
-        for (int m = 0; m <= L + 2; m++) {
+        const int nz = L + 3;
+        if (lane < (u32)nz) ztot[lane] = 0u;
+        if (lane + 32 < (u32)nz) ztot[lane + 32] = 0u;
+        __syncwarp();
+#pragma unroll 8
+        for (int m = 0; m < nz; m++) {
             const u32 w0 = (u32)m * (n / 32);
             const bool in = (w0 + lane) * 32u < U.WU;
             sh[m][lane] = in ? hib[w0 + lane] : 0u;
             sl[m][lane] = in ? lob[w0 + lane] : 0u;
-            u32 c = 0;
-            for (u32 j = lane; j < tpz; j += 32) {
-                const u32 tt = (u32)m * tpz + j;
-                c += tt < U.NTU ? chi[tt] : 0u;
-            }
-#pragma unroll
-            for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-            if (lane == 0) ztot[m] = c;
         }
+        for (u32 tt = lane; tt < (u32)nz * tpz && tt < U.NTU; tt += 32) atomicAdd(&ztot[tt / tpz], chi[tt]);
         __syncwarp();
     }
     u32 s = 0;
