@@ -289,8 +289,9 @@ class OracleSample:
 # ------------------------------------------------------------- roofline
 
 def roofline_traffic(workload: str, kernel: str):
-    """DRAM bytes per launch of `kernel` from the committed ncu capture of
-    the same workload (profiles/r02_roofline_traffic.json)."""
+    """DRAM bytes of one captured launch of `kernel` (ncu --set full, same
+    workload) and that launch's algorithmic bytes
+    (profiles/r02_roofline_traffic.json, from profiles/r02_ncu_*)."""
     try:
         with open(os.path.join(ROOT, "profiles", "r02_roofline_traffic.json")) as fh:
             return json.load(fh).get(workload, {}).get(kernel)
@@ -329,8 +330,10 @@ def roofline_entry(kind: int, rec: dict, peaks: dict, ipk: dict | None, workload
     tr = roofline_traffic(workload, "modup" if kind == PROBE_MODUP else "ks_inner")
     e = {"kernel": PROBE_NAMES[kind], "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
          "unit": "GB/s", "frac": round(achieved / peak, 4),
-         "traffic": tr["dram_bytes_per_launch"] if tr else None,
-         "traffic_source": tr["source"] if tr else None,
+         "traffic": int(tr["dram_bytes_per_launch"]) if tr else None,
+         "traffic_vs_algorithmic": round(tr["dram_bytes_per_launch"] / tr["algorithmic_bytes_per_launch"], 3)
+         if tr else None,
+         "traffic_source": (tr["source"] + "; captured launch: " + tr["launch"]) if tr else None,
          "launches_timed": int(rec["launches"]), "launch_ms": round(launch_ms, 4),
          "algorithmic_bytes_per_launch": int(rec["bytes"] / launches),
          "share_of_step": round(rec["ms"] / step_ms_total, 4),

@@ -764,8 +764,11 @@ static void modup_and_inner(const Dev& d, int B, int l, u64* D, u64* E, const u6
     if (!fused) {
         const double jobs = (double)B * (l + 1) * (l + 1), n = d.n;
         {
-            // algorithmic bytes: each pass reads and writes one limb per job
-            ProbeScope ps(PROBE_MODUP, st, jobs * 32.0 * n, jobs * (n / 2) * d.log_n, 2);
+            // algorithmic (unique) bytes: pass A reads each digit once (its l+1
+            // lifts re-read it from L2) and writes one limb per job; pass B
+            // reads and writes one limb per job
+            ProbeScope ps(PROBE_MODUP, st, (3.0 * jobs + (double)B * (l + 1)) * 8.0 * n,
+                          jobs * (n / 2) * d.log_n, 2);
             launch_ntt<true>(d, JobModUp{D, E, l, d.L, d.n, d.pc}, B * (l + 1) * (l + 1), st);
         }
         {
@@ -1144,7 +1147,7 @@ bool rotate_accumulate_grouped(const Dev& d, int B, int G, const int* gs, const 
     launch_ntt<false>(d, JobDecompose<SrcPerm>{SrcPerm{ct, gal}, E, D, d.df, l, n, d}, B * (l + 1), st);
     {
         const double jobs = (double)G * (l + 1) * l + (double)B * (l + 1), nn = n;
-        ProbeScope ps(PROBE_MODUP, st, jobs * 32.0 * nn, jobs * (nn / 2) * d.log_n, 4);
+        ProbeScope ps(PROBE_MODUP, st, (3.0 * jobs + 2.0 * B * (l + 1)) * 8.0 * nn, jobs * (nn / 2) * d.log_n, 4);
         launch_ntt<true>(d, JobModUpAux{D, E, l, d.L, n, d.pc}, B * (l + 1), st);
         group_sum_kernel<<<dim3((n + 255) / 256, l + 1, G), 256, 0, st>>>(d, l, gs, D, E);
         note_launch();
