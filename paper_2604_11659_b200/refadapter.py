@@ -42,9 +42,16 @@ class ReferenceBridge:
         p = ref_ctx.params
         self.params = CkksParams(ring_degree=p.ring_degree, modulus_chain=tuple(p.modulus_chain),
                                  scale_bits=p.scale_bits, aux_prime=p.aux_prime, seed=p.seed)
-        self.ctx = CkksContext(self.params, device_index)
+        self._device_index = device_index
+        self._ctx = None                # the device context, created on first execute
         self._uploaded = set()          # ("relin", id) / ("galois", step)
         self._masks = {}                # (id(mask_cache), pos) -> device tensor (Montgomery)
+
+    @property
+    def ctx(self) -> CkksContext:
+        if self._ctx is None:
+            self._ctx = CkksContext(self.params, self._device_index)
+        return self._ctx
 
     # -- key material: uploaded once per key, converted to Montgomery form on device
     def _sync_keys(self, keys, steps) -> None:
@@ -62,69 +69,87 @@ class ReferenceBridge:
             self.ctx.upload_key(1, r, _key_array(gk))
             self._uploaded.add(("galois", r))
 
-    def _mask_table(self, mask_cache, positions):
-        L = self.params.levels
-        n = self.params.ring_degree
-        for pos in positions:
-            key = (id(mask_cache), int(pos))
-            if key in self._masks:
-                continue
-            pt = mask_cache.get(int(pos))
-            t = D.to_dev(np.ascontiguousarray(np.stack(pt.limbs), dtype=np.uint64))
-            check(lib().hs_to_montgomery(self.ctx.handle, D.ptr(t), 1, L, 0, 0, D.stream()))
-            self._masks[key] = t
-        npos = int(max(positions)) + 1 if len(positions) else 1
-        arr = (ctypes.c_void_p * npos)()
-        for pos in positions:
-            arr[int(pos)] = self._masks[(id(mask_cache), int(pos))].data_ptr()
-        del n
-        return arr, npos
-
-    def spmm_csr_csc(self, enc_a, enc_b, ctx, keys, counter=None, mask_cache=None):
-        ref_engine = sys.modules[type(counter).__module__] if counter is not None else None
+    # -- the three halves of one call (extract and wrap are pure host code,
+    # tested with the genuine reference objects in tests/test_bridge_reference.py)
+    def extract(self, enc_a, enc_b, ctx, counter=None, mask_cache=None) -> dict:
+        """Read the reference objects: layout check (engine.py:167-173), the
+        CSR x CSC schedule (C++ planner), the Galois steps it needs, the mask
+        limbs of its slots and both ciphertexts as uint64 arrays."""
         ref_encmat = sys.modules[type(enc_a).__module__]
         if enc_a.meta.layout.value != "csr" or enc_b.meta.layout.value != "csc":
             raise ref_encmat.ParameterError(
                 f"layout mismatch: need csr x csc, got {enc_a.meta.layout.value} x "
                 f"{enc_b.meta.layout.value}")
         dim = enc_a.dim
+        ref_engine = sys.modules[ref_encmat.__name__.replace("encmat", "engine")]
         if counter is None:
-            counter = sys.modules[ref_encmat.__name__.replace("encmat", "engine")].OpCounter()
+            counter = ref_engine.OpCounter()
         if mask_cache is None:
-            mask_cache = sys.modules[ref_encmat.__name__.replace("encmat", "engine")].MaskCache(ctx, dim)
-        start = time.perf_counter()
+            mask_cache = ref_engine.MaskCache(ctx, dim)
         from .encmat import plan_csr_csc
-        pairs = plan_csr_csc(enc_a.meta, enc_b.meta)
+        pairs = np.ascontiguousarray(plan_csr_csc(enc_a.meta, enc_b.meta), dtype=np.int64).reshape(-1, 4)
         slots = self.params.slots
-        L = self.params.levels
         steps = set()
         if len(pairs):
             ap, bp = pairs[:, 2], pairs[:, 3]
             al = np.abs(ap - bp)
             rot = np.minimum(ap, bp) - (pairs[:, 0] * dim + pairs[:, 1])
             steps = {int(x) % slots for x in np.unique(np.concatenate([al[al != 0], rot[rot != 0]]))}
-        self._sync_keys(keys, sorted(steps))
-        positions = np.unique(np.minimum(pairs[:, 2], pairs[:, 3])) if len(pairs) else []
-        table, npos = self._mask_table(mask_cache, positions)
-        ca = D.to_dev(np.ascontiguousarray(np.array(enc_a.ctxt.polys, dtype=np.uint64)))
-        cb = D.to_dev(np.ascontiguousarray(np.array(enc_b.ctxt.polys, dtype=np.uint64)))
-        out = D.empty((2, L - 1, self.params.ring_degree))
-        cnt = HsCounters()
-        pl = np.ascontiguousarray(pairs, dtype=np.int64)
-        check(lib().hs_spmspm_pairs(self.ctx.handle, dim, pl.ctypes.data_as(c_i64p), len(pl),
-                                    D.ptr(ca), D.ptr(cb), table, npos, D.ptr(out),
-                                    ctypes.byref(cnt), 0, 1, D.stream()))
-        res_np = D.to_host(out)
+        positions = np.unique(np.minimum(pairs[:, 2], pairs[:, 3])) if len(pairs) else np.zeros(0, np.int64)
+        masks = {int(p): np.ascontiguousarray(np.stack(mask_cache.get(int(p)).limbs), dtype=np.uint64)
+                 for p in positions}
+        return {"dim": dim, "pairs": pairs, "steps": sorted(steps), "masks": masks,
+                "ct_a": np.ascontiguousarray(np.array(enc_a.ctxt.polys, dtype=np.uint64)),
+                "ct_b": np.ascontiguousarray(np.array(enc_b.ctxt.polys, dtype=np.uint64)),
+                "counter": counter, "mask_cache": mask_cache, "encmat": ref_encmat}
+
+    def wrap(self, x: dict, enc_a, enc_b, ctx, res: np.ndarray | None, counts: dict, seconds: float):
+        """The reference's own result types, counter increments,
+        ctx.relin_noops and counter.wall_time (engine.py:136-184)."""
+        counter, ref_encmat = x["counter"], x["encmat"]
         for name in ("ct_ct_mults", "pt_mults", "rotations", "relins", "relin_noops", "rescales",
                      "adds", "alignment_rotations", "accumulation_rotations"):
-            setattr(counter, name, getattr(counter, name) + getattr(cnt, name))
-        ctx.relin_noops += cnt.relin_noops
-        counter.wall_time += time.perf_counter() - start
-        del ref_engine
-        if not cnt.has_result:
+            setattr(counter, name, getattr(counter, name) + int(counts[name]))
+        ctx.relin_noops += int(counts["relin_noops"])
+        counter.wall_time += seconds
+        dim = x["dim"]
+        if res is None:
             return ref_encmat.EncryptedResult(ctxt=None, dim=dim)
+        L = self.params.levels
         chain = self.params.modulus_chain
         scale = ((enc_a.ctxt.scale * enc_b.ctxt.scale) / chain[L] * float(chain[L - 1])) / chain[L - 1]
-        ct_type = type(enc_a.ctxt)
-        polys = tuple(tuple(res_np[p, i] for i in range(L - 1)) for p in range(2))
-        return ref_encmat.EncryptedResult(ctxt=ct_type(polys, scale, L - 2), dim=dim)
+        polys = tuple(tuple(res[p, i] for i in range(L - 1)) for p in range(2))
+        return ref_encmat.EncryptedResult(ctxt=type(enc_a.ctxt)(polys, scale, L - 2), dim=dim)
+
+    def execute(self, x: dict, keys):
+        """Device half: keys and masks uploaded once, the runner over the
+        extracted schedule.  Returns (result [2][L-1][n] or None, counts)."""
+        self._sync_keys(keys, x["steps"])
+        positions = list(x["masks"])
+        for pos in positions:
+            key = (id(x["mask_cache"]), pos)
+            if key not in self._masks:
+                t = D.to_dev(x["masks"][pos])
+                check(lib().hs_to_montgomery(self.ctx.handle, D.ptr(t), 1, self.params.levels, 0, 0,
+                                             D.stream()))
+                self._masks[key] = t
+        npos = max(positions) + 1 if positions else 1
+        table = (ctypes.c_void_p * npos)()
+        for pos in positions:
+            table[pos] = self._masks[(id(x["mask_cache"]), pos)].data_ptr()
+        L = self.params.levels
+        ca, cb = D.to_dev(x["ct_a"]), D.to_dev(x["ct_b"])
+        out = D.empty((2, L - 1, self.params.ring_degree))
+        cnt = HsCounters()
+        pl = x["pairs"]
+        check(lib().hs_spmspm_pairs(self.ctx.handle, x["dim"], pl.ctypes.data_as(c_i64p), len(pl),
+                                    D.ptr(ca), D.ptr(cb), table, npos, D.ptr(out),
+                                    ctypes.byref(cnt), 0, 1, D.stream()))
+        counts = {name: getattr(cnt, name) for name, _ in HsCounters._fields_}
+        return (D.to_host(out) if cnt.has_result else None), counts
+
+    def spmm_csr_csc(self, enc_a, enc_b, ctx, keys, counter=None, mask_cache=None):
+        start = time.perf_counter()
+        x = self.extract(enc_a, enc_b, ctx, counter, mask_cache)
+        res, counts = self.execute(x, keys)
+        return self.wrap(x, enc_a, enc_b, ctx, res, counts, time.perf_counter() - start)

@@ -4,7 +4,10 @@ The real reference package cannot travel to the GPU box, so reference-typed
 objects are built here with the same attribute surface (SURVEY.md §8b
 "duck-typed inputs") from CPU-oracle data, in a module named like the
 reference's (`<pkg>.encmat` / `<pkg>.engine`).  The bridge must return the
-oracle's result bit for bit, in the reference's own result types.
+oracle's result bit for bit, in the reference's own result types.  The host
+halves of the bridge (extract / wrap) are checked against the GENUINE
+reference objects and the reference's own runner in the build container
+(tests/test_bridge_reference.py).
 """
 
 import sys
