@@ -32,6 +32,7 @@ namespace {
 
 struct PlanPair {
     int64_t i, j, ap, bp;
+    int32_t k = 0;         // operand product (hs_spmspm_multi): operands cta[k], ctb[k]
 };
 
 u32 norm_step(int64_t s, u32 slots) {
@@ -222,14 +223,14 @@ struct KeyProvider {
 // step) rotated at level L into outs[k]; per source one decomposition + ModUp
 // per chunk of steps (chunks bounded by the work budget and, for generated
 // keys, by the key pool).
-static hs_status compute_alignments(hs_ctx* c, const u64* ct_a, const u64* ct_b,
+static hs_status compute_alignments(hs_ctx* c, const std::vector<const u64*>& operands,
                                     const std::vector<std::pair<int, u32>>& todo,
                                     const std::vector<u64*>& outs_all, KeyProvider& KP, DeviceArena& A,
                                     size_t budget, int64_t max_gen, cudaStream_t st) {
     const int L = c->L;
     const u32 n = c->n;
     const Dev& d = c->dev;
-    for (int src = 0; src < 2; src++) {
+    for (int src = 0; src < (int)operands.size(); src++) {
         std::vector<u32> gal, steps_src;
         std::vector<const u64*> keys;
         std::vector<const u64*> outs;
@@ -260,7 +261,7 @@ static hs_status compute_alignments(hs_ctx* c, const u64* ct_a, const u64* ct_b,
         }
         HS_CUDA(cudaMemcpyAsync(d_gal, gal.data(), R * sizeof(u32), cudaMemcpyHostToDevice, st));
         HS_CUDA(cudaMemcpyAsync(d_outs, outs.data(), R * sizeof(u64*), cudaMemcpyHostToDevice, st));
-        const u64* sp = src ? ct_b : ct_a;
+        const u64* sp = operands[src];
         for (int r0 = 0; r0 < R; r0 += (int)rmax) {
             const int rc = std::min<int>((int)rmax, R - r0);
             std::vector<u32> chunk(steps_src.begin() + r0, steps_src.begin() + r0 + rc);
@@ -281,8 +282,12 @@ static hs_status compute_alignments(hs_ctx* c, const u64* ct_a, const u64* ct_b,
     return HS_OK;
 }
 
-hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, const u64* ct_a,
-                    const u64* ct_b, const u64* const* masks, int64_t nmasks, u64* out,
+// Operand product k of a pair: ct_a = cta[k], ct_b = ctb[k] (one product for
+// the plain runner; the products of one tiled output block otherwise).
+// Alignment rotations are deduplicated per (operand, step), operand id 2k+src.
+hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs,
+                    const std::vector<const u64*>& cta, const std::vector<const u64*>& ctb,
+                    const u64* const* masks, int64_t nmasks, u64* out,
                     hs_counters* cnt, int shard, int nshard, cudaStream_t st,
                     std::chrono::steady_clock::time_point t_start) {
     const int L = c->L;
@@ -318,11 +323,15 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, cons
     }
     for (int64_t p = 0; p < np; p++) {
         const PlanPair& q = pairs[p];
+        if (q.k < 0 || q.k >= (int32_t)cta.size()) {
+            set_error("pair operand product index out of range");
+            return (hs_status)HS_PARAMETER_ERROR;
+        }
         int64_t mn;
         ia[p] = 0;
         ib[p] = 1;
         if (q.ap != q.bp) {
-            const int src = q.ap < q.bp ? 1 : 0;          // the higher-positioned operand rotates
+            const int src = (q.ap < q.bp ? 1 : 0) + 2 * q.k;  // the higher-positioned operand rotates
             const int64_t raw = q.ap < q.bp ? q.bp - q.ap : q.ap - q.bp;
             const u32 r = norm_step(raw, slots);
             C.rotations++;
@@ -339,7 +348,7 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, cons
                 } else {
                     idx = it->second;
                 }
-                (src ? ib[p] : ia[p]) = idx;
+                ((src & 1) ? ib[p] : ia[p]) = idx;
             }
             mn = std::min(q.ap, q.bp);
         } else {
@@ -436,7 +445,12 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, cons
         if (ks_ != HS_OK) return ks_;
     }
     {
-        hs_status s_ = compute_alignments(c, ct_a, ct_b, todo, todo_out, KP, A, budget, max_gen, st);
+        std::vector<const u64*> operands;
+        for (size_t k = 0; k < cta.size(); k++) {
+            operands.push_back(cta[k]);
+            operands.push_back(ctb[k]);
+        }
+        hs_status s_ = compute_alignments(c, operands, todo, todo_out, KP, A, budget, max_gen, st);
         if (s_ != HS_OK) return s_;
     }
 
@@ -445,8 +459,8 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs, cons
     std::vector<u32> hG(P);
     for (int64_t t = 0; t < P; t++) {
         const int64_t p = order[lo + t];
-        hA[t] = ia[p] >= 2 ? align_ptr[ia[p]] : ct_a;
-        hB[t] = ib[p] >= 2 ? align_ptr[ib[p]] : ct_b;
+        hA[t] = ia[p] >= 2 ? align_ptr[ia[p]] : cta[pairs[p].k];
+        hB[t] = ib[p] >= 2 ? align_ptr[ib[p]] : ctb[pairs[p].k];
         hM[t] = masks[mpos[p]];
         hG[t] = accr[p] ? (u32)powmod_h(5, accr[p], 2ull * n) : 0u;
     }
@@ -623,7 +637,7 @@ hs_status hs_spmspm_csr_csc(hs_ctx* c, int32_t dim, const int64_t* oa, const int
     const auto t0 = std::chrono::steady_clock::now();
     std::vector<PlanPair> pairs;
     merge_pairs(dim, oa, ia, ob, ib, [&](const PlanPair& p) { pairs.push_back(p); });
-    return run_pairs(c, dim, pairs, ct_a, ct_b, masks, nmasks, out, counters, shard, nshard,
+    return run_pairs(c, dim, pairs, {ct_a}, {ct_b}, masks, nmasks, out, counters, shard, nshard,
                      (cudaStream_t)stream, t0);
 }
 
@@ -634,7 +648,24 @@ hs_status hs_spmspm_pairs(hs_ctx* c, int32_t dim, const int64_t* pl, int64_t np,
     const auto t0 = std::chrono::steady_clock::now();
     std::vector<PlanPair> pairs(np);
     for (int64_t p = 0; p < np; p++) pairs[p] = PlanPair{pl[4 * p], pl[4 * p + 1], pl[4 * p + 2], pl[4 * p + 3]};
-    return run_pairs(c, dim, pairs, ct_a, ct_b, masks, nmasks, out, counters, shard, nshard,
+    return run_pairs(c, dim, pairs, {ct_a}, {ct_b}, masks, nmasks, out, counters, shard, nshard,
+                     (cudaStream_t)stream, t0);
+}
+
+hs_status hs_spmspm_multi(hs_ctx* c, int32_t dim, const int64_t* pl, int64_t np, const uint64_t* const* cts_a,
+                          const uint64_t* const* cts_b, int32_t nprod, const uint64_t* const* masks,
+                          int64_t nmasks, uint64_t* out, hs_counters* counters, int32_t shard, int32_t nshard,
+                          void* stream) {
+    const auto t0 = std::chrono::steady_clock::now();
+    if (nprod < 1) {
+        set_error("hs_spmspm_multi: no operand products");
+        return (hs_status)HS_PARAMETER_ERROR;
+    }
+    std::vector<PlanPair> pairs(np);
+    for (int64_t p = 0; p < np; p++)
+        pairs[p] = PlanPair{pl[5 * p], pl[5 * p + 1], pl[5 * p + 2], pl[5 * p + 3], (int32_t)pl[5 * p + 4]};
+    return run_pairs(c, dim, pairs, std::vector<const u64*>(cts_a, cts_a + nprod),
+                     std::vector<const u64*>(cts_b, cts_b + nprod), masks, nmasks, out, counters, shard, nshard,
                      (cudaStream_t)stream, t0);
 }
 
@@ -697,7 +728,7 @@ hs_status hs_align_compute(hs_ctx* c, const uint64_t* ct_a, const uint64_t* ct_b
         hs_status s = KP.init((int)(2 * max_gen));
         if (s != HS_OK) return s;
     }
-    hs_status s = compute_alignments(c, ct_a, ct_b, todo, o, KP, A, c->batch_bytes, max_gen, st);
+    hs_status s = compute_alignments(c, {ct_a, ct_b}, todo, o, KP, A, c->batch_bytes, max_gen, st);
     if (s != HS_OK) return s;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {

@@ -124,15 +124,29 @@ def required_rotation_steps_tiled(ta: TiledMatrix, tb: TiledMatrix) -> set:
 
 def spmm_tiled(ta: TiledMatrix, tb: TiledMatrix, ctx, keys, counter=None, mask_cache=None,
                spmm=None) -> TiledResult:
-    """Block SpMSpM: every non-empty A[I][K] x B[K][J] on the engine, partial
-    products of an output block summed with eval_add (counted as adds)."""
-    from .engine import MaskCache, OpCounter, spmm_csr_csc
+    """Block SpMSpM.  Default: one runner call per output block C[I][J]
+    over all its products A[I][K] x B[K][J] (engine.run_products:
+    hs_spmspm_multi schedules their pairs together, so a Galois key is
+    generated once per step for the block, and the products' sum is the
+    runner's own modular accumulation).  With ``spmm`` given (e.g. the
+    multi-GPU runner), every non-empty product runs on it and the partial
+    products of a block are joined with eval_add.  Both are bit-identical,
+    with the same logical counters (the joins count as adds)."""
+    from .engine import MaskCache, OpCounter, run_products
     if ta.layout is not Layout.CSR or tb.layout is not Layout.CSC:
         raise ParameterError("tiled product needs CSR x CSC operands")
     counter = counter if counter is not None else OpCounter()
     mask_cache = mask_cache if mask_cache is not None else MaskCache(ctx, ta.b)
-    spmm = spmm if spmm is not None else spmm_csr_csc
     res = TiledResult(n=ta.n, T=ta.T, b=ta.b)
+    if spmm is None:
+        blocks: dict = {}
+        for I, K, J in block_products(ta, tb):
+            blocks.setdefault((I, J), []).append((ta.tiles[(I, K)], tb.tiles[(K, J)]))
+        for key in sorted(blocks):
+            part = run_products(blocks[key], ctx, keys, counter, mask_cache)
+            if part.ctxt is not None:
+                res.tiles[key] = part
+        return res
     for I, K, J in block_products(ta, tb):
         part = spmm(ta.tiles[(I, K)], tb.tiles[(K, J)], ctx, keys, counter, mask_cache)
         if part.ctxt is None:

@@ -34,8 +34,11 @@ def _numpy_draws(params, seed, r):
     return a, e
 
 
+# the last set is the north-star ring at L = 24: 6 keys x 25 digits x 65,536
+# normals (~9.8 M ziggurat draws, ~120 K slow-path exp / log1p evaluations) and
+# 6 x 650 uniform segments, raw draws compared with numpy itself
 @pytest.mark.parametrize("n,sb,L,nkeys", [(64, 40, 2, 5), (1024, 45, 2, 5), (16384, 50, 2, 5), (8192, 40, 4, 5),
-                                          (4096, 50, 6, 24)])
+                                          (4096, 50, 6, 24), (65536, 50, 24, 6)])
 def test_device_stream_replays_numpy(pkg, n, sb, L, nkeys):
     from paper_2604_11659_b200 import device as D
     from paper_2604_11659_b200._lib import check, lib

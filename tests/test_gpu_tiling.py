@@ -81,3 +81,22 @@ def test_block_products_bit_exact_vs_oracle(setup, oracle_mod):
     assert set(want) == set(res.tiles)
     for key, w in want.items():
         assert np.array_equal(res.tiles[key].ctxt.host(), w), key
+
+
+def test_block_runner_equals_per_product_runs(setup):
+    """One hs_spmspm_multi call per output block (the default) == every
+    product on the plain runner joined with eval_add: same limbs, scale,
+    level and logical counters."""
+    P, ctx, keys, a, b, ta, tb, _ = setup
+    from paper_2604_11659_b200 import engine, tiling
+    c1, c2 = engine.OpCounter(), engine.OpCounter()
+    fused = tiling.spmm_tiled(ta, tb, ctx, keys, c1)
+    plain = tiling.spmm_tiled(ta, tb, ctx, keys, c2, spmm=engine.spmm_csr_csc)
+    assert sorted(fused.tiles) == sorted(plain.tiles)
+    for k in fused.tiles:
+        f, p = fused.tiles[k].ctxt, plain.tiles[k].ctxt
+        assert np.array_equal(f.host(), p.host()), k
+        assert f.scale == p.scale and f.level == p.level
+    for name in ("ct_ct_mults", "pt_mults", "rotations", "relins", "relin_noops", "rescales", "adds",
+                 "alignment_rotations", "accumulation_rotations"):
+        assert getattr(c1, name) == getattr(c2, name), name
