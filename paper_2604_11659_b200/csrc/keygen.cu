@@ -1615,6 +1615,9 @@ struct JobKeyFused {
         return (neg && t) ? P.q - t : t;
     }
     HS_DEV u64* scratch(const Ctx& c) const { return c.b; }
+    HS_DEV void prefetch(const Ctx& c, u32 j) const {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(c.a + j));
+    }
     HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst& P) const {
         u64 acc = csub(csub(v, P.two_q), P.q);
         // f = 0 for the aux modulus (m = L+1): one code path

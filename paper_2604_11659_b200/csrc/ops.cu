@@ -278,6 +278,9 @@ struct JobDecompose {                       // inverse NTT, job = b*(l+1)+i
     }
 };
 
+#ifndef HS_LIFT_LAZY
+#define HS_LIFT_LAZY 1           // ModUp loaders lift into [0, 4q) (approximate Barrett)
+#endif
 struct JobModUp {                           // forward NTT, job = (b*(l+1)+i)*(l+1)+t
     const u64* D;
     u64* E;
@@ -302,7 +305,11 @@ struct JobModUp {                           // forward NTT, job = (b*(l+1)+i)*(l
     }
     HS_DEV int prime(const Ctx& c) const { return c.pm; }
     HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst& P) const {
+#if HS_LIFT_LAZY
+        return lift_lazy(__ldg(c.d + j), c.qsrc, P);           // [0, 4q): forward loader
+#else
         return lift_mod_sel(__ldg(c.d + j), c.qsrc, P, c.small);
+#endif
     }
     HS_DEV u64* scratch(const Ctx& c) const { return c.e; }
     // E stays in [0, 4q): the inner product only needs sum_i e k < 2^128 with
@@ -1100,7 +1107,13 @@ struct JobModUpAux {                         // forward NTT, job = b*(l+1)+i: th
         return Ctx{D + (size_t)jb * n, E + ((size_t)jb * (l + 2) + l + 1) * n, pc[i].q};
     }
     HS_DEV int prime(const Ctx&) const { return L + 1; }
-    HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst& P) const { return lift_mod(__ldg(c.d + j), c.qsrc, P); }
+    HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst& P) const {
+#if HS_LIFT_LAZY
+        return lift_lazy(__ldg(c.d + j), c.qsrc, P);
+#else
+        return lift_mod(__ldg(c.d + j), c.qsrc, P);
+#endif
+    }
     HS_DEV u64* scratch(const Ctx& c) const { return c.e; }
     HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst&) const { c.e[j] = v; }
 };
