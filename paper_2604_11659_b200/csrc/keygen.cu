@@ -1611,20 +1611,23 @@ struct JobKeyFused {
     HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst& P) const {
         const long long v = __ldg(c.e + j);
         const bool neg = v < 0;                               // |v| mod q, then negate: one path
-        const u64 t = reduce64(neg ? (u64)(-(v + 1)) + 1ull : (u64)v, P);
+        u64 t = neg ? (u64)(-(v + 1)) + 1ull : (u64)v;
+        // e = rint(3.2 x) of a ziggurat normal: |e| < 64 << q in practice
+        // (the tail's x stays below ~14); the reduction is a never-taken branch
+        if (t >= P.q) t = reduce64(t, P);
         return (neg && t) ? P.q - t : t;
     }
     HS_DEV u64* scratch(const Ctx& c) const { return c.b; }
-    HS_DEV void prefetch(const Ctx& c, u32 j) const {
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(c.a + j));
-    }
+    // b = NTT(e) + f sk(X^g) - a sk, with f = p (Q_L / q_i) mod q_m nonzero only
+    // for m == i (a warp-uniform branch), reduced once at the end:
+    // v in [0, 4q), a sk in [0, 2q) -> v + 2q - a sk in (0, 6q), + f sk' < 8q
     HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst& P) const {
-        u64 acc = csub(csub(v, P.two_q), P.q);
-        // f = 0 for the aux modulus (m = L+1): one code path
-        acc = add_mod(acc, shoup(__ldg(c.skpm + j), c.f.x, c.f.y, P.q), P.q);
-        // a * sk with sk's Shoup companion (stored after the L+2 sk limbs)
-        const u64 ask = csub(shoup_lazy(__ldg(c.a + j), __ldg(c.skm + j), __ldg(c.skm + (size_t)(L + 2) * d.n + j), P.q), P.q);
-        c.b[j] = sub_mod(acc, ask, P.q);
+        const u64 ask = shoup_lazy(__ldg(c.a + j), __ldg(c.skm + j), __ldg(c.skm + (size_t)(L + 2) * d.n + j), P.q);
+        u64 r = v + P.two_q - ask;
+        if (c.f.x) r += shoup_lazy(__ldg(c.skpm + j), c.f.x, c.f.y, P.q);
+        r = csub(r, P.two_q << 1);
+        r = csub(r, P.two_q);
+        c.b[j] = csub(r, P.q);
     }
 };
 

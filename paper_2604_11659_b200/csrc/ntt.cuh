@@ -332,13 +332,6 @@ constexpr int kIoUnroll = NTT_IO_UNROLL;   // (#pragma arguments are not macro-e
 #define NTT_NBUF 1             // A/B cfg2|cfg3s: 2 -> 125.0|892 ms, 1 -> 123.0|856, 1 + 8 CTAs/SM -> 120.5|850
 #endif
 
-// Optional Job::prefetch(ctx, j): L2 prefetch of the epilogue's streamed
-// operand line starting at element j (see PassEngine::run).
-template <class J, class = void>
-struct HasPrefetch { static constexpr bool value = false; };
-template <class J>
-struct HasPrefetch<J, std::void_t<decltype(&J::prefetch)>> { static constexpr bool value = true; };
-
 // LOGN (log2 ring degree) and S0 (first stage of the pass) are template
 // parameters so every index shift/mask below is a compile-time constant.
 template <bool FWD, bool FIRST, bool LAST, int LOGG, int H, int C, int EPT, int LOGN, int S0, class Job>
@@ -449,13 +442,7 @@ struct PassEngine {
         u64 v[EPT];
         using MF = RM<RFIRST>;
         using ML = RM<RLAST>;
-        // jobs whose epilogue streams another operand from DRAM (JobKeyFused:
-        // the key's a half) get its lines pulled into L2 before the
-        // butterflies, so the epilogue's loads hit L2 (row passes: the
-        // tile is contiguous, one 128-byte line per thread)
-        if constexpr (LAST && C == 1 && HasPrefetch<Job>::value) {
-            if (E.t * 16u < (u32)TILE) job.prefetch(E.jc, E.gidx(0, 0, 0) + E.t * 16u);
-        }
+
         // ---- load
         if constexpr (MF::direct && !(FIRST && NTT_STAGED_FIRST)) {
             constexpr u32 gstride = 1u << (MF::LOWB + LO_BITS);
