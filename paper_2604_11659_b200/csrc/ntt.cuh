@@ -59,6 +59,9 @@ HS_DEV u64 mulhi_apx(u64 x, u64 y) {
 // x*w - Q*q is formed as x*w + Q*(2^64 - q) (nq) so the chain is pure IMADs.
 HS_DEV u64 shoup_ex(u64 x, u64 w, u64 w_sh, u64 nq) { return x * w + mulhi_ex(x, w_sh) * nq; }
 
+#ifndef NTT_SHOUP_CC
+#define NTT_SHOUP_CC 1
+#endif
 // Approximate-quotient Shoup product in 11 IMADs (all on the FMA pipe; the
 // 64-bit accumulations use IMAD.WIDE with a unit multiplier so no register
 // pair has to be assembled with MOVs):
@@ -73,12 +76,24 @@ HS_DEV u64 shoup_ax(u64 x, u64 w, u64 w_sh, u64 nq) {
         "mov.b64 {w0, w1}, %2;\n\t"
         "mov.b64 {s0, s1}, %3;\n\t"
         "mov.b64 {n0, n1}, %4;\n\t"
+#if NTT_SHOUP_CC
+        // Q = x1 s1 + hi(x1 s0) + hi(x0 s1): the two high halves added into
+        // the low word with carry (mad.hi.cc + addc): no zero-extended 64-bit
+        // addends, so no register moves on the FMA pipe
+        "mul.wide.u32 Q, x1, s1;\n\t"
+        "mov.b64 {q0, q1}, Q;\n\t"
+        "mad.hi.cc.u32 q0, x1, s0, q0;\n\t"
+        "addc.u32 q1, q1, 0;\n\t"
+        "mad.hi.cc.u32 q0, x0, s1, q0;\n\t"
+        "addc.u32 q1, q1, 0;\n\t"
+#else
         "mul.hi.u32 a, x1, s0;\n\t"
         "mul.hi.u32 b, x0, s1;\n\t"
         "mul.wide.u32 Q, x1, s1;\n\t"
         "mad.wide.u32 Q, a, 1, Q;\n\t"
         "mad.wide.u32 Q, b, 1, Q;\n\t"
         "mov.b64 {q0, q1}, Q;\n\t"
+#endif
         "mul.wide.u32 T, x0, w0;\n\t"
         "mad.wide.u32 T, q0, n0, T;\n\t"
         "mov.b64 {t0, t1}, T;\n\t"
