@@ -299,7 +299,7 @@ def roofline_traffic(workload: str, kernel: str):
         return None
 
 
-PROBE_MODUP, PROBE_KS_INNER = 1, 2
+PROBE_MODUP, PROBE_KS_INNER, PROBE_KEYGEN = 1, 2, 3
 PROBE_NAMES = {PROBE_MODUP: "ntt_pass_kernel<JobModUp> (ModUp NTT passes of the key switch)",
                PROBE_KS_INNER: "ks_inner_kernel (key inner product)"}
 
@@ -507,7 +507,7 @@ def run_b200_arm(args, wl):
         one_step()
 
     # ---- timed region: K executions; kernel probes armed inside it
-    check(lib().hs_probe_arm((1 << PROBE_MODUP) | (1 << PROBE_KS_INNER)))
+    check(lib().hs_probe_arm((1 << PROBE_MODUP) | (1 << PROBE_KS_INNER) | (1 << PROBE_KEYGEN)))
     launches0 = lib().hs_launch_count()
     dev_ms, e2e_ms, same = 0.0, 0.0, True
     d2h = 0
@@ -520,6 +520,7 @@ def run_b200_arm(args, wl):
             same &= bool(np.array_equal(out, first))
     launches = lib().hs_launch_count() - launches0
     probes = {k: probe_read(k) for k in (PROBE_MODUP, PROBE_KS_INNER)}
+    kg = probe_read(PROBE_KEYGEN)
     check(lib().hs_probe_arm(0))
     if world > 1:
         t = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64, device="cuda")
@@ -571,6 +572,11 @@ def run_b200_arm(args, wl):
             "roofline_other": other,
             "ks_hbm_floor": ks_floor,
             "int_peak": ipk,
+            "keygen": {"keys_per_step": int(kg["work"] / args.steps),
+                       "ms_per_step": round(kg["ms"] / args.steps, 1),
+                       "ms_per_key": round(kg["ms"] / kg["work"], 4) if kg["work"] else None,
+                       "note": "device Galois-key generation inside the step, timed on its side "
+                               "stream (overlaps the pair work on the main stream)"},
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "result_repeatable": same,

@@ -62,7 +62,8 @@ int64_t hs_launch_count(void);
 /* Measurement hooks for bench.py's roofline line (no reference counterpart).
  * hs_probe_arm(mask): every later launch of an armed kernel class (bit k of
  * mask arms kind k: 1 = the ModUp NTT passes of the key switch, 2 = the key
- * inner product; 0 = off) records a CUDA event pair on its own launching
+ * inner product, 3 = one device key-generation call; 0 = off) records a
+ * CUDA event pair on its own launching
  * stream; arming clears the record.  hs_probe_read(kind, out4) synchronises
  * on those events and returns {launches, total ms, algorithmic DRAM bytes,
  * integer work (butterflies resp. 64x64-bit MACs)} of that kind.

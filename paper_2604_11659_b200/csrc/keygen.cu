@@ -1808,6 +1808,9 @@ hs_status generate_galois_keys(hs_ctx* c, const std::vector<u32>& steps,
         // room for KG_LANES sub-chunk slices, each 256-byte aligned
         HS_CUDA(cudaMallocAsync(&par_scratch, keygen_par_scratch_bytes(KB, c->n, c->L) + hs_ctx::KG_LANES * 512, st));
     }
+    // in-step timer (bench.py): the whole generation of these keys on its stream;
+    // bytes = the keys written, work = keys
+    ProbeScope probe(PROBE_KEYGEN, st, (double)steps.size() * c->key_bytes(), (double)steps.size());
     for (size_t k0 = 0; k0 < steps.size(); k0 += KB) {
         const int K = (int)std::min<size_t>(KB, steps.size() - k0);
         std::vector<u64*> keys(K), aout(K);

@@ -862,8 +862,8 @@ struct JobModDownRescale {                   // forward NTT, job = (b*2+c)*l+m, 
     }
     HS_DEV int prime(const Ctx& c) const { return c.m; }
     HS_DEV u64 load(const Ctx& c, u32 j, const PrimeConst& P) const {
-        const u64 tp = shoup_lazy(lift_mod(__ldg(c.t + j), d.aux_q, P), c.wp.x, c.wp.y, P.q);   // [0, 2q)
-        return tp + lift_mod(__ldg(c.u + j), c.ql, P);                                           // [0, 3q)
+        const u64 tp = shoup_lazy(lift_lazy(__ldg(c.t + j), d.aux_q, P), c.wp.x, c.wp.y, P.q);  // [0, 2q)
+        return csub(tp + lift_lazy(__ldg(c.u + j), c.ql, P), P.two_q);                          // [0, 4q)
     }
     HS_DEV u64* scratch(const Ctx& c) const { return c.out; }
     HS_DEV void store(const Ctx& c, u32 j, u64 v, const PrimeConst& P) const {

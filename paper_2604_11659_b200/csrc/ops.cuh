@@ -30,7 +30,7 @@ long long launch_count();
 // pair on its own launching stream around it, with the launch's algorithmic
 // DRAM bytes and integer work (butterflies or 64x64 MACs).  hs_probe_read
 // synchronises and returns {launches, total ms, bytes, work}.
-enum ProbeKind { PROBE_NONE = 0, PROBE_MODUP = 1, PROBE_KS_INNER = 2, PROBE_KINDS = 3 };
+enum ProbeKind { PROBE_NONE = 0, PROBE_MODUP = 1, PROBE_KS_INNER = 2, PROBE_KEYGEN = 3, PROBE_KINDS = 4 };
 struct ProbeScope {
     int slot = -1;
     cudaStream_t st;
