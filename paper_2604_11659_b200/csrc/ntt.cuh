@@ -59,9 +59,6 @@ HS_DEV u64 mulhi_apx(u64 x, u64 y) {
 // x*w - Q*q is formed as x*w + Q*(2^64 - q) (nq) so the chain is pure IMADs.
 HS_DEV u64 shoup_ex(u64 x, u64 w, u64 w_sh, u64 nq) { return x * w + mulhi_ex(x, w_sh) * nq; }
 
-#ifndef NTT_SMEM_TW
-#define NTT_SMEM_TW 1
-#endif
 #ifndef NTT_SHOUP_CC
 #define NTT_SHOUP_CC 1
 #endif
@@ -524,16 +521,7 @@ ntt_pass_kernel(Dev d, Job job, int jbase) {
     const int p = job.prime(E.jc);
     E.P = d.pc[p];
     E.tw = (FWD ? d.tw : d.itw) + ((size_t)p << LOGN);
-#if NTT_SMEM_TW
-    // a pass over the first stages (S0 = 0) only uses twiddles [1, 2^LOGG):
-    // staged once per CTA in shared memory (LDS instead of 64-bit-addressed LDG)
-    if constexpr (S0 == 0 && LOGG <= 9 && LOGN > LOGG) {
-        __shared__ ulonglong2 s_tw[1 << LOGG];
-        for (u32 k = threadIdx.x; k < (1u << LOGG); k += blockDim.x) s_tw[k] = __ldg(E.tw + k);
-        __syncthreads();
-        E.tw = s_tw;
-    }
-#endif
+
     constexpr u32 ncolblk = (1u << PE::LO_BITS) / C;
     E.hi0 = (blockIdx.x / ncolblk) * H;
     E.lo0 = (blockIdx.x % ncolblk) * C;
