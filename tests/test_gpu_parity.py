@@ -451,3 +451,57 @@ def test_owned_alignments_across_simulated_ranks(pkg, world):
     summed = torch.stack(parts).sum(0)
     check(lib().hs_reduce_mod(ctx.handle, D.ptr(summed), 2, L - 1, D.stream()))
     assert np.array_equal(D.to_host(summed.view(torch.uint64)), _arr(full.ctxt))
+
+
+def _dist_worker(rank, world, port, q):
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2604_11659_b200 as P
+        from paper_2604_11659_b200 import dist as hdist
+        from paper_2604_11659_b200 import engine
+        out = product_runner_case(P, 1024, 45, 2, 2024, 16, 0.5, 1 * 1_000_003 + 16 * 1_009)
+        ea, eb, ctx, keys, mc = out[5], out[6], out[1], out[2], out[9]
+        c = engine.OpCounter()
+        res = hdist.spmm_csr_csc_distributed(ea, eb, ctx, keys, c, mc)
+        q.put((rank, res.ctxt.host().tobytes(), c.physical_alignment, c.ct_ct_mults))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_runner_multiprocess(pkg, world):
+    """The whole multi-GPU path (dist.spmm_csr_csc_distributed: shard plan,
+    owned alignments computed once, point-to-point exchange, shard runs, SUM
+    all-reduce, mod-q) in `world` processes -- on one GPU, so the collectives
+    run over gloo (device tensors staged through host memory) -- equals the
+    single-process runner bit for bit, and no alignment is computed twice."""
+    import socket
+    import torch.multiprocessing as mp
+    from paper_2604_11659_b200 import dist as hdist
+    params, ctx, keys, a, b, ea, eb, full, counter, mc = product_runner_case(
+        pkg, 1024, 45, 2, 2024, 16, 0.5, 1 * 1_000_003 + 16 * 1_009)
+    plan = hdist.plan_shards(hdist._plan_pairs(ea, eb), 16, params.slots, world)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx_mp = mp.get_context("spawn")
+    q = ctx_mp.Queue()
+    procs = [ctx_mp.Process(target=_dist_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    want = _arr(full.ctxt)
+    for rank, blob, phys, mults in got:
+        assert np.array_equal(np.frombuffer(blob, dtype=np.uint64).reshape(want.shape), want), rank
+        assert mults == counter.ct_ct_mults
+    # every rank computed exactly the alignments it owns (the runner recomputed none)
+    owned = np.bincount(plan["owner"], minlength=world)
+    assert {g[0]: g[2] for g in got} == {r: int(owned[r]) for r in range(world)}
