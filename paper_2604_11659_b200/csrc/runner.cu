@@ -227,57 +227,75 @@ static hs_status compute_alignments(hs_ctx* c, const std::vector<const u64*>& op
                                     const std::vector<std::pair<int, u32>>& todo,
                                     const std::vector<u64*>& outs_all, KeyProvider& KP, DeviceArena& A,
                                     size_t budget, int64_t max_gen, cudaStream_t st) {
+    // Chunks of distinct STEPS across all source operands: each chunk's keys
+    // are acquired once and serve every operand rotated by those steps (at
+    // cfg3, 2,963 rotations share 1,544 steps: per-operand chunks generated
+    // 1,419 of those keys twice).
     const int L = c->L;
     const u32 n = c->n;
     const Dev& d = c->dev;
-    for (int src = 0; src < (int)operands.size(); src++) {
-        std::vector<u32> gal, steps_src;
-        std::vector<const u64*> keys;
-        std::vector<const u64*> outs;
-        for (size_t k = 0; k < todo.size(); k++) {
-            const auto& al = todo[k];
-            if (al.first != src) continue;
-            gal.push_back((u32)powmod_h(5, al.second, 2ull * n));
-            steps_src.push_back(al.second);
-            outs.push_back(outs_all[k]);
-        }
-        keys.assign(gal.size(), nullptr);
-        const int R = (int)gal.size();
-        if (!R) continue;
-        const size_t base_e = ks_hoisted_scratch_elems(0, L, n);
-        const size_t per_e = ks_hoisted_scratch_elems(1, L, n) - base_e;
-        int64_t rmax = budget / 8 > base_e ? (int64_t)((budget / 8 - base_e) / per_e) : 1;
-        rmax = std::max<int64_t>(1, std::min<int64_t>(rmax, R));
-        bool any_gen = false;
-        for (u32 r : steps_src) any_gen |= !KP.resident(r);
-        if (any_gen) rmax = std::min<int64_t>(rmax, max_gen);
-        u64* scratch = A.get<u64>(ks_hoisted_scratch_elems((int)rmax, L, n));
-        u32* d_gal = A.get<u32>(R);
-        const u64** d_keys = A.get<const u64*>(R);
-        const u64** d_outs = A.get<const u64*>(R);
-        if (A.failed) {
-            set_error("out of device memory (alignment)");
-            return (hs_status)HS_OUT_OF_MEMORY;
-        }
-        HS_CUDA(cudaMemcpyAsync(d_gal, gal.data(), R * sizeof(u32), cudaMemcpyHostToDevice, st));
-        HS_CUDA(cudaMemcpyAsync(d_outs, outs.data(), R * sizeof(u64*), cudaMemcpyHostToDevice, st));
-        const u64* sp = operands[src];
-        for (int r0 = 0; r0 < R; r0 += (int)rmax) {
-            const int rc = std::min<int>((int)rmax, R - r0);
-            std::vector<u32> chunk(steps_src.begin() + r0, steps_src.begin() + r0 + rc);
-            std::vector<const u64*> kp;
-            hs_status ks_ = KP.acquire(chunk, kp);
+    const int R = (int)todo.size();
+    if (!R) return HS_OK;
+    std::vector<u32> steps;                                  // distinct, first-use order
+    {
+        std::unordered_map<u32, int> seen;
+        for (const auto& al : todo)
+            if (seen.emplace(al.second, 0).second) steps.push_back(al.second);
+    }
+    const size_t base_e = ks_hoisted_scratch_elems(0, L, n);
+    const size_t per_e = ks_hoisted_scratch_elems(1, L, n) - base_e;
+    int64_t rmax = budget / 8 > base_e ? (int64_t)((budget / 8 - base_e) / per_e) : 1;
+    rmax = std::max<int64_t>(1, std::min<int64_t>(rmax, (int64_t)steps.size()));
+    bool any_gen = false;
+    for (u32 r : steps) any_gen |= !KP.resident(r);
+    if (any_gen) rmax = std::min<int64_t>(rmax, max_gen);
+    u64* scratch = A.get<u64>(ks_hoisted_scratch_elems((int)rmax, L, n));
+    u32* d_gal = A.get<u32>(R);
+    const u64** d_keys = A.get<const u64*>(R);
+    const u64** d_outs = A.get<const u64*>(R);
+    if (A.failed) {
+        set_error("out of device memory (alignment)");
+        return (hs_status)HS_OUT_OF_MEMORY;
+    }
+    std::vector<u32> hgal(R);
+    std::vector<const u64*> hkeys(R), houts(R);
+    int used = 0;                                            // entries of the device arrays filled
+    const int nchunks = (int)((steps.size() + rmax - 1) / rmax);
+    for (int ci = 0; ci < nchunks; ci++) {
+        const size_t s0 = (size_t)ci * rmax, s1 = std::min(steps.size(), s0 + (size_t)rmax);
+        std::vector<u32> chunk(steps.begin() + s0, steps.begin() + s1);
+        std::unordered_map<u32, int> kidx;
+        for (size_t k = 0; k < chunk.size(); k++) kidx[chunk[k]] = (int)k;
+        std::vector<const u64*> kp;
+        hs_status ks_ = KP.acquire(chunk, kp);
+        if (ks_ != HS_OK) return ks_;
+        if (any_gen && ci + 1 < nchunks && prefetch_on()) {   // next chunk's keys while this one computes
+            const size_t n0 = s1, n1 = std::min(steps.size(), s1 + (size_t)rmax);
+            ks_ = KP.prefetch(std::vector<u32>(steps.begin() + n0, steps.begin() + n1), chunk);
             if (ks_ != HS_OK) return ks_;
-            if (any_gen && r0 + rc < R && prefetch_on()) {   // next chunk's keys while this one computes
-                const int rn = std::min<int>((int)rmax, R - r0 - rc);
-                ks_ = KP.prefetch(std::vector<u32>(steps_src.begin() + r0 + rc,
-                                                   steps_src.begin() + r0 + rc + rn), chunk);
-                if (ks_ != HS_OK) return ks_;
-            }
-            HS_CUDA(cudaMemcpyAsync(d_keys + r0, kp.data(), rc * sizeof(u64*), cudaMemcpyHostToDevice, st));
-            rotate_hoisted(d, rc, L, sp, d_gal + r0, d_keys + r0, table(d_outs + r0), scratch, st);
-            KP.release(chunk);
         }
+        for (int src = 0; src < (int)operands.size(); src++) {
+            const int r0 = used;
+            for (int k = 0; k < R; k++) {
+                const auto& al = todo[k];
+                if (al.first != src) continue;
+                auto it = kidx.find(al.second);
+                if (it == kidx.end()) continue;
+                hgal[used] = (u32)powmod_h(5, al.second, 2ull * n);
+                hkeys[used] = kp[it->second];
+                houts[used] = outs_all[k];
+                used++;
+            }
+            const int rc = used - r0;
+            if (!rc) continue;
+            HS_CUDA(cudaMemcpyAsync(d_gal + r0, hgal.data() + r0, rc * sizeof(u32), cudaMemcpyHostToDevice, st));
+            HS_CUDA(cudaMemcpyAsync(d_keys + r0, hkeys.data() + r0, rc * sizeof(u64*), cudaMemcpyHostToDevice,
+                                    st));
+            HS_CUDA(cudaMemcpyAsync(d_outs + r0, houts.data() + r0, rc * sizeof(u64*), cudaMemcpyHostToDevice,
+                                    st));
+            rotate_hoisted(d, rc, L, operands[src], d_gal + r0, d_keys + r0, table(d_outs + r0), scratch, st);
+        }
+        KP.release(chunk);
     }
     return HS_OK;
 }
