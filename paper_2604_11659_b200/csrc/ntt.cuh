@@ -76,7 +76,15 @@ HS_DEV u64 shoup_ax(u64 x, u64 w, u64 w_sh, u64 nq) {
         "mov.b64 {w0, w1}, %2;\n\t"
         "mov.b64 {s0, s1}, %3;\n\t"
         "mov.b64 {n0, n1}, %4;\n\t"
-#if NTT_SHOUP_CC
+#if NTT_SHOUP_CC == 2
+        // as below, with x1 s1 as mul.lo + mul.hi (no IMAD.WIDE for Q)
+        "mul.lo.u32 q0, x1, s1;\n\t"
+        "mul.hi.u32 q1, x1, s1;\n\t"
+        "mad.hi.cc.u32 q0, x1, s0, q0;\n\t"
+        "addc.u32 q1, q1, 0;\n\t"
+        "mad.hi.cc.u32 q0, x0, s1, q0;\n\t"
+        "addc.u32 q1, q1, 0;\n\t"
+#elif NTT_SHOUP_CC
         // Q = x1 s1 + hi(x1 s0) + hi(x0 s1): the two high halves added into
         // the low word with carry (mad.hi.cc + addc): no zero-extended 64-bit
         // addends, so no register moves on the FMA pipe
