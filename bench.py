@@ -334,6 +334,7 @@ def roofline_entry(kind: int, rec: dict, peaks: dict, ipk: dict | None, workload
          "traffic_vs_algorithmic": round(tr["dram_bytes_per_launch"] / tr["algorithmic_bytes_per_launch"], 3)
          if tr else None,
          "traffic_source": (tr["source"] + "; captured launch: " + tr["launch"]) if tr else None,
+         "binding_pipe": tr.get("binding_pipe") if tr else None,
          "launches_timed": int(rec["launches"]), "launch_ms": round(launch_ms, 4),
          "algorithmic_bytes_per_launch": int(rec["bytes"] / launches),
          "share_of_step": round(rec["ms"] / step_ms_total, 4),
