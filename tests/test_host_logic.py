@@ -115,3 +115,18 @@ def test_shard_plan_owns_each_alignment_once_and_balances():
                 used = {int(pl["pair_align"][p]) for p in pl["order"][lo:hi] if pl["pair_align"][p] >= 0}
                 assert sorted(used) == pl["need"][r]
             assert sum(hi - lo for lo, hi in pl["ranges"]) == len(pairs)
+
+
+def test_shard_plan_edge_cases():
+    """More ranks than pairs, no alignment at all, a single rank."""
+    from paper_2604_11659_b200 import dist
+    pairs = np.array([[0, 0, 0, 0], [0, 1, 1, 1]], dtype=np.int64)          # no alignment rotations
+    pl = dist.plan_shards(pairs, 4, 32, 5)
+    assert len(pl["align"]) == 0 and all(n == [] for n in pl["need"])
+    assert sum(hi - lo for lo, hi in pl["ranges"]) == 2
+    pairs = np.array([[0, 0, 0, 3], [1, 0, 2, 5], [0, 1, 4, 3]], dtype=np.int64)
+    pl = dist.plan_shards(pairs, 4, 32, 1)
+    assert list(pl["owner"]) == [0] * len(pl["align"])
+    assert pl["need"][0] == list(range(len(pl["align"])))
+    pl = dist.plan_shards(np.zeros((0, 4), dtype=np.int64), 4, 32, 3)
+    assert pl["ranges"] == [(0, 0)] * 3 and len(pl["align"]) == 0
