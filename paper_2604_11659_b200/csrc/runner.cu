@@ -401,16 +401,6 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs,
     const int64_t P = hi - lo;
     C.pairs = P;
 
-    // alignments this shard needs, compacted
-    std::vector<char> seen(2 + align_list.size(), 0);
-    std::vector<int32_t> need;
-    for (int64_t t = lo; t < hi; t++) {
-        for (int32_t idx : {ia[order[t]], ib[order[t]]})
-            if (idx >= 2 && !seen[idx]) {
-                seen[idx] = 1;
-                need.push_back(idx);
-            }
-    }
     const auto t_plan = std::chrono::steady_clock::now();
     C.plan_ms = std::chrono::duration<double, std::milli>(t_plan - t_start).count();
 
@@ -421,13 +411,73 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs,
         *cnt = C;
         return (hs_status)HS_OK;
     }
-
-    DeviceArena A{st};
-    KeyProvider KP{c, st};
     const size_t budget = c->batch_bytes;
     // generated keys per chunk/batch: the key pool holds two such sets (the
     // one in use and the one being prefetched), bounded by twice the budget
     const int64_t max_gen = std::max<int64_t>(1, (int64_t)(budget / c->key_bytes()));
+
+    // The aligned operands of a range live in HBM for the whole range (one
+    // ct at level L each: 25 MiB at N=2^16, L=24; 72 MiB at 2^17, L=35).
+    // When all of them do not fit next to the batch work and the key pool,
+    // the step-sorted pair list runs in consecutive ranges whose aligned
+    // operands fit (their alignments recomputed per range; the output is
+    // one modular sum either way).
+    int64_t amax = INT64_MAX;
+    {
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+            const size_t pool = c->kpool_buf.size() >= (size_t)(2 * max_gen) ? 0
+                              : (size_t)(2 * max_gen) * c->key_bytes();
+            const size_t reserve = 2 * budget + pool + ((size_t)2 << 30);
+            amax = free_b > reserve ? (int64_t)((free_b - reserve) / (ctL * sizeof(u64))) : 1;
+            amax = std::max<int64_t>(1, amax);
+        }
+        static const long long cap_env = getenv("HS_ALIGN_MAX") ? atoll(getenv("HS_ALIGN_MAX")) : 0;
+        if (cap_env > 0) amax = std::min<int64_t>(amax, cap_env);        // A/B and tests: force ranges
+    }
+    std::vector<int64_t> cuts{lo};
+    {
+        std::vector<char> seen(2 + align_list.size(), 0);
+        int64_t cnt_a = 0;
+        for (int64_t t = lo; t < hi; t++) {
+            int64_t add = 0;
+            for (int32_t idx : {ia[order[t]], ib[order[t]]})
+                if (idx >= 2 && !seen[idx] && !c->ext_align.count((u64)align_list[idx - 2].first * slots +
+                                                                   align_list[idx - 2].second))
+                    add++;
+            if (cnt_a + add > amax && t > cuts.back()) {
+                cuts.push_back(t);
+                std::fill(seen.begin(), seen.end(), 0);
+                cnt_a = 0;
+                add = 0;
+                for (int32_t idx : {ia[order[t]], ib[order[t]]})
+                    if (idx >= 2 && !c->ext_align.count((u64)align_list[idx - 2].first * slots +
+                                                        align_list[idx - 2].second))
+                        add++;
+            }
+            for (int32_t idx : {ia[order[t]], ib[order[t]]})
+                if (idx >= 2) seen[idx] = 1;
+            cnt_a += add;
+        }
+        cuts.push_back(hi);
+    }
+    C.physical_alignment = 0;
+    bool lazy_used = false;
+
+    // one range of the step-sorted pairs: its alignments, then its pair batches
+    auto run_range = [&](const int64_t lo, const int64_t hi) -> hs_status {
+    const int64_t P = hi - lo;
+    std::vector<char> seen(2 + align_list.size(), 0);
+    std::vector<int32_t> need;
+    for (int64_t t = lo; t < hi; t++) {
+        for (int32_t idx : {ia[order[t]], ib[order[t]]})
+            if (idx >= 2 && !seen[idx]) {
+                seen[idx] = 1;
+                need.push_back(idx);
+            }
+    }
+    DeviceArena A{st};
+    KeyProvider KP{c, st};
 
     // ---- phase 1: hoisted alignment rotations (those another rank computed
     // and handed over with hs_align_provide are used as they are)
@@ -453,7 +503,7 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs,
         todo.push_back(align_list[idx - 2]);
         todo_out.push_back(o);
     }
-    C.physical_alignment = (int64_t)todo.size();
+    C.physical_alignment += (int64_t)todo.size();
     bool lazy_needed = false;
     for (const auto& al : todo) lazy_needed |= !c->galois.count(al.second);
     for (int64_t t = lo; t < hi && !lazy_needed; t++)
@@ -613,12 +663,20 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs,
         }
         KP.release(bsteps);
     }
+    lazy_used |= lazy_needed;
+    return (hs_status)HS_OK;
+    };
+
+    for (size_t ci = 0; ci + 1 < cuts.size(); ci++) {
+        hs_status s_ = run_range(cuts[ci], cuts[ci + 1]);
+        if (s_ != HS_OK) return s_;
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         set_error(std::string("kernel launch failed: ") + cudaGetErrorString(e));
         return (hs_status)HS_CUDA_ERROR;
     }
-    if (lazy_needed) {            // generated keys must have come from complete streams
+    if (lazy_used) {              // generated keys must have come from complete streams
         HS_CUDA(cudaStreamSynchronize(st));
         hs_status ks_ = keygen_check(c);
         if (ks_ != HS_OK) return ks_;
