@@ -120,6 +120,13 @@ hs_status hs_keygen_streams(hs_ctx* ctx, const uint64_t* pcg_states, int32_t nke
                             int64_t* e_out, void* stream);
 int64_t hs_keys_generated(const hs_ctx* ctx);
 /* Standard-form copy [2][L+1][L+2][n] into device buffer `out`. */
+/* A key switching key straight from a reference HESP container record
+ * (ckks/serial.py:48-66: u32 digits, per digit the b and a polys, each a u32
+ * count and count x (u32 size, 8n bytes)) already copied to the device as
+ * raw bytes (4-byte aligned): one gather kernel writes the key -- no host
+ * unpacking of the per-limb records. */
+hs_status hs_key_upload_hesp(hs_ctx* ctx, int kind, uint32_t step, const uint8_t* record, int64_t record_bytes,
+                             void* stream);
 hs_status hs_key_download(hs_ctx* ctx, int kind, uint32_t step, uint64_t* out, void* stream);
 int hs_key_has(const hs_ctx* ctx, int kind, uint32_t step);
 hs_status hs_key_drop(hs_ctx* ctx, int kind, uint32_t step);

@@ -47,6 +47,7 @@ _SIGS = {
     "hs_key_generate": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_uint32, c_vp, c_vp, c_vp, c_vp,
                                        c_vp]),
     "hs_key_download": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_uint32, c_vp, c_vp]),
+    "hs_key_upload_hesp": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_uint32, c_vp, ctypes.c_int64, c_vp]),
     "hs_keygen_set_tables": (ctypes.c_int, [c_vp, ctypes.POINTER(ctypes.c_double),
                                             ctypes.POINTER(ctypes.c_double), c_u64p]),
     "hs_keygen_set_secret": (ctypes.c_int, [c_vp, c_vp, c_vp]),

@@ -334,6 +334,54 @@ hs_status hs_key_upload(hs_ctx* c, int kind, uint32_t step, const uint64_t* key,
     return (hs_status)HS_OK;
 }
 
+}  // extern "C"
+
+namespace hs {
+// HESP container KSK record (reference ckks/serial.py:48-66): u32 digits,
+// then per digit the b poly and the a poly, each = u32 count followed by
+// count x (u32 byte size = 8n, 8n bytes of little-endian uint64 limbs).
+// Limbs sit at 4-byte (not 8-byte) alignment, so words are read as u32 pairs.
+__global__ void hesp_ksk_gather_kernel(const unsigned* raw, u64* key, int L, u32 n) {
+    const u32 j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const int limb = blockIdx.y;                       // (c * (L+1) + i) * (L+2) + m
+    const int m = limb % (L + 2), ci = limb / (L + 2);
+    const int i = ci % (L + 1), c = ci / (L + 1);
+    const size_t limb_rec = 4 + (size_t)8 * n;          // bytes
+    const size_t poly_rec = 4 + (size_t)(L + 2) * limb_rec;
+    const size_t off = 4 + (size_t)i * 2 * poly_rec + (size_t)c * poly_rec + 4 + (size_t)m * limb_rec + 4 +
+                       (size_t)8 * j;                   // bytes from the record start
+    const unsigned* w = raw + off / 4;
+    key[(size_t)limb * n + j] = (u64)w[0] | ((u64)w[1] << 32);
+}
+}  // namespace hs
+
+extern "C" {
+
+hs_status hs_key_upload_hesp(hs_ctx* c, int kind, uint32_t step, const uint8_t* rec, int64_t rec_bytes,
+                             void* stream) {
+    if (!key_args_ok(c, kind, step)) return (hs_status)HS_PARAMETER_ERROR;
+    const int L = c->L;
+    const u32 n = c->n;
+    const size_t limb_rec = 4 + (size_t)8 * n, poly_rec = 4 + (size_t)(L + 2) * limb_rec;
+    const size_t need = 4 + (size_t)(L + 1) * 2 * poly_rec;
+    if ((size_t)rec_bytes != need || ((uintptr_t)rec & 3)) {
+        set_error("hs_key_upload_hesp: record size " + std::to_string(rec_bytes) + " != " +
+                  std::to_string(need) + " (or misaligned)");
+        return (hs_status)HS_PARAMETER_ERROR;
+    }
+    KeyBuf* kb = key_slot(c, kind, step, true);
+    if (!kb) {
+        set_error("out of device memory for key");
+        return (hs_status)HS_OUT_OF_MEMORY;
+    }
+    hesp_ksk_gather_kernel<<<dim3((n + 255) / 256, 2 * (L + 1) * (L + 2)), 256, 0, ST(stream)>>>(
+        (const unsigned*)rec, kb->d, L, n);
+    note_launch();
+    CHECK_LAUNCH();
+    return (hs_status)HS_OK;
+}
+
 hs_status hs_key_generate(hs_ctx* c, int kind, uint32_t step, const uint64_t* a, const int64_t* e,
                           const uint64_t* target, const uint64_t* sk, void* stream) {
     if (!key_args_ok(c, kind, step)) return (hs_status)HS_PARAMETER_ERROR;
