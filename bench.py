@@ -500,10 +500,21 @@ def run_b200_arm(args, wl):
         out = result_host(res)
         t1 = time.perf_counter()
         torch.cuda.synchronize()
+        last_res[0] = res
         return out, c, e0.elapsed_time(e1), (t1 - t0) * 1e3
 
+    last_res = [None]
     first, c, _, _ = one_step()
     assert c.ct_ops() == ct_ops, (c.ct_ops(), ct_ops)
+    # accuracy of the decrypted product vs the plaintext matmul (the reference's
+    # acceptance bound: Frobenius error < 1e-6, tests/test_acceptance.py:30)
+    from paper_2604_11659_b200 import formats
+    if tiled:
+        dec = tiling.decrypt_tiled(last_res[0], ctx, keys)
+    else:
+        dec = encmat.decrypt_result(last_res[0], ctx, keys)
+    plain = formats.as_dense(a) @ formats.as_dense(b)
+    frob = float(np.sqrt(np.sum((np.asarray(dec) - plain) ** 2)))
     for _ in range(max(0, args.warmup - 1)):
         one_step()
 
@@ -581,6 +592,9 @@ def run_b200_arm(args, wl):
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "result_repeatable": same,
+            "accuracy": {"frobenius_vs_plaintext": frob, "tolerance": 1e-6, "ok": frob < 1e-6,
+                         "note": "decrypted result of the first execution vs plain_matmul "
+                                 "(the reference's acceptance bound, tests/test_acceptance.py:30-31)"},
         }
         print(json.dumps(line), flush=True)
     if world > 1:
