@@ -221,18 +221,20 @@ hs_status hs_spmspm_pairs(hs_ctx* ctx, int32_t dim, const int64_t* pairs, int64_
                           const uint64_t* const* masks, int64_t nmasks, uint64_t* out,
                           hs_counters* counters, int32_t shard_index, int32_t shard_count,
                           void* stream);
-/* Several operand products summed into ONE output (multi-ciphertext tiling,
- * beyond the reference's one-ciphertext capacity, encmat.py:131-133): output
- * block C[I][J] = sum_K A[I][K] B[K][J] in one call.  pairs are (i, j, a_pos,
- * b_pos, k) rows, k indexing cts_a[k] / cts_b[k]; all pairs are scheduled
- * together (sorted by accumulation step across the products), so a Galois
- * key is generated once per step for the whole block.  Logical counters:
- * the sum of the products' counts plus the (products - 1) joining adds. */
+/* Several operand products accumulated into one or more outputs in ONE
+ * schedule (multi-ciphertext tiling, beyond the reference's one-ciphertext
+ * capacity, encmat.py:131-133): output block C[I][J] = sum_K A[I][K] B[K][J]
+ * for every block at once.  pairs are (i, j, a_pos, b_pos, k, o) rows: k
+ * indexes cts_a[k] / cts_b[k], o the output outs[o].  All pairs are
+ * scheduled together (sorted by accumulation step across products and
+ * outputs), so a Galois key is generated once per step for the whole tiled
+ * product and alignment rotations are deduplicated per (operand, step).
+ * Logical counters: the products' counts plus the joining adds (adds =
+ * pairs - outputs with a pair). */
 hs_status hs_spmspm_multi(hs_ctx* ctx, int32_t dim, const int64_t* pairs, int64_t npairs,
                           const uint64_t* const* cts_a, const uint64_t* const* cts_b, int32_t nproducts,
-                          const uint64_t* const* masks, int64_t nmasks, uint64_t* out,
-                          hs_counters* counters, int32_t shard_index, int32_t shard_count,
-                          void* stream);
+                          const uint64_t* const* masks, int64_t nmasks, uint64_t* const* outs, int32_t noutputs,
+                          hs_counters* counters, int32_t shard_index, int32_t shard_count, void* stream);
 
 /* Alignment rotations shared across ranks (multi-GPU, dist.py).  The CSR/C
  * runner rotates the higher-positioned operand of a pair by |a_pos - b_pos|

@@ -95,8 +95,8 @@ _SIGS = {
                                        c_vp]),
     "hs_spmspm_multi": (ctypes.c_int, [c_vp, ctypes.c_int32, c_i64p, ctypes.c_int64, ctypes.POINTER(c_vp),
                                        ctypes.POINTER(c_vp), ctypes.c_int32, ctypes.POINTER(c_vp),
-                                       ctypes.c_int64, c_vp, ctypes.POINTER(HsCounters), ctypes.c_int32,
-                                       ctypes.c_int32, c_vp]),
+                                       ctypes.c_int64, ctypes.POINTER(c_vp), ctypes.c_int32,
+                                       ctypes.POINTER(HsCounters), ctypes.c_int32, ctypes.c_int32, c_vp]),
     "hs_reduce_mod": (ctypes.c_int, [c_vp, c_vp, ctypes.c_int32, ctypes.c_int32, c_vp]),
     "hs_set_batch_bytes": (None, [c_vp, ctypes.c_uint64]),
     "hs_align_compute": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.POINTER(ctypes.c_int32),

@@ -33,6 +33,7 @@ namespace {
 struct PlanPair {
     int64_t i, j, ap, bp;
     int32_t k = 0;         // operand product (hs_spmspm_multi): operands cta[k], ctb[k]
+    int32_t o = 0;         // output ciphertext (hs_spmspm_multi): outs[o]
 };
 
 u32 norm_step(int64_t s, u32 slots) {
@@ -305,7 +306,7 @@ static hs_status compute_alignments(hs_ctx* c, const std::vector<const u64*>& op
 // Alignment rotations are deduplicated per (operand, step), operand id 2k+src.
 hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs,
                     const std::vector<const u64*>& cta, const std::vector<const u64*>& ctb,
-                    const u64* const* masks, int64_t nmasks, u64* out,
+                    const u64* const* masks, int64_t nmasks, const std::vector<u64*>& outs,
                     hs_counters* cnt, int shard, int nshard, cudaStream_t st,
                     std::chrono::steady_clock::time_point t_start) {
     const int L = c->L;
@@ -341,8 +342,8 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs,
     }
     for (int64_t p = 0; p < np; p++) {
         const PlanPair& q = pairs[p];
-        if (q.k < 0 || q.k >= (int32_t)cta.size()) {
-            set_error("pair operand product index out of range");
+        if (q.k < 0 || q.k >= (int32_t)cta.size() || q.o < 0 || q.o >= (int32_t)outs.size()) {
+            set_error("pair operand product / output index out of range");
             return (hs_status)HS_PARAMETER_ERROR;
         }
         int64_t mn;
@@ -389,14 +390,25 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs,
     }
     C.ct_ct_mults = C.pt_mults = C.relins = C.relin_noops = np;
     C.rescales = 2 * np;
-    C.adds = np > 0 ? np - 1 : 0;
+    {
+        // one accumulator per output: adds = pairs - (outputs with a pair)
+        std::vector<char> has(outs.size(), 0);
+        int64_t nonempty = 0;
+        for (const PlanPair& q : pairs)
+            if (!has[q.o]) {
+                has[q.o] = 1;
+                nonempty++;
+            }
+        C.adds = np - nonempty;
+    }
     C.has_result = np > 0;
 
     // ---- shard: pairs sorted by accumulation step, contiguous ranges
     std::vector<int64_t> order(np);
     std::iota(order.begin(), order.end(), 0);
-    std::stable_sort(order.begin(), order.end(),
-                     [&](int64_t x, int64_t y) { return accr[x] < accr[y]; });
+    std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) {
+        return accr[x] != accr[y] ? accr[x] < accr[y] : pairs[x].o < pairs[y].o;
+    });
     const int64_t lo = np * shard / nshard, hi = np * (shard + 1) / nshard;
     const int64_t P = hi - lo;
     C.pairs = P;
@@ -406,7 +418,7 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs,
 
     const size_t ctL = (size_t)2 * (L + 1) * n;           // ct at level L
     const size_t ctL2 = (size_t)2 * (L - 1) * n;          // ct at level L-2
-    HS_CUDA(cudaMemsetAsync(out, 0, ctL2 * sizeof(u64), st));
+    for (u64* o : outs) HS_CUDA(cudaMemsetAsync(o, 0, ctL2 * sizeof(u64), st));
     if (P == 0) {
         *cnt = C;
         return (hs_status)HS_OK;
@@ -523,19 +535,53 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs,
     }
 
     // ---- phase 2: pair batches
+    const size_t per_pair = ks_scratch_elems(1, L, n) +
+                            (size_t)n * (2 * (L + 1) + 2 * L + 4 * (L - 1) + 2);
+    int64_t B = std::max<int64_t>(1, std::min<int64_t>((int64_t)(budget / 8 / per_pair), P));
+    B = std::min<int64_t>(B, 8192);
+    // batches over the step-sorted range: up to B pairs and at most max_gen
+    // distinct non-resident keys
+    std::vector<int64_t> bstart;
+    std::vector<std::vector<u32>> bsteps_all;
+    for (int64_t s = 0, bnext; s < P; s = bnext) {
+        std::vector<u32> bsteps;
+        int64_t ngen = 0;
+        bnext = s;
+        while (bnext < P && bnext - s < B) {
+            const u32 r = accr[order[lo + bnext]];
+            if (r && (bsteps.empty() || bsteps.back() != r)) {
+                const bool lazy = !KP.resident(r);
+                if (lazy && ngen + 1 > max_gen && bnext > s) break;
+                bsteps.push_back(r);
+                ngen += lazy;
+            }
+            bnext++;
+        }
+        bstart.push_back(s);
+        bsteps_all.push_back(bsteps);
+    }
+    bstart.push_back(P);
+    // several outputs (tiled blocks): within a batch, items of one output
+    // are made contiguous (then by step), so each output's accumulation runs
+    // once per batch while the batch's keys serve every output
+    if (outs.size() > 1)
+        for (size_t bi = 0; bi + 1 < bstart.size(); bi++)
+            std::stable_sort(order.begin() + lo + bstart[bi], order.begin() + lo + bstart[bi + 1],
+                             [&](int64_t x, int64_t y) {
+                                 return pairs[x].o != pairs[y].o ? pairs[x].o < pairs[y].o : accr[x] < accr[y];
+                             });
     std::vector<const u64*> hA(P), hB(P), hM(P), hK(P);
-    std::vector<u32> hG(P);
+    std::vector<u32> hG(P), hR(P);
+    std::vector<int32_t> hO(P);
     for (int64_t t = 0; t < P; t++) {
         const int64_t p = order[lo + t];
         hA[t] = ia[p] >= 2 ? align_ptr[ia[p]] : cta[pairs[p].k];
         hB[t] = ib[p] >= 2 ? align_ptr[ib[p]] : ctb[pairs[p].k];
         hM[t] = masks[mpos[p]];
         hG[t] = accr[p] ? (u32)powmod_h(5, accr[p], 2ull * n) : 0u;
+        hR[t] = accr[p];
+        hO[t] = pairs[p].o;
     }
-    const size_t per_pair = ks_scratch_elems(1, L, n) +
-                            (size_t)n * (2 * (L + 1) + 2 * L + 4 * (L - 1) + 2);
-    int64_t B = std::max<int64_t>(1, std::min<int64_t>((int64_t)(budget / 8 / per_pair), P));
-    B = std::min<int64_t>(B, 8192);
     const u64** dA = A.get<const u64*>(P);
     const u64** dB = A.get<const u64*>(P);
     const u64** dM = A.get<const u64*>(P);
@@ -559,11 +605,9 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs,
     HS_CUDA(cudaMemcpyAsync(dG, hG.data(), P * sizeof(u32), cudaMemcpyHostToDevice, st));
     HS_CUDA(cudaMemcpyAsync(dR, relin_rep.data(), B * sizeof(u64*), cudaMemcpyHostToDevice, st));
 
-    std::vector<u32> hR(P);
-    for (int64_t t = 0; t < P; t++) hR[t] = accr[order[lo + t]];
     // key runs of each batch's rotated items (rotate_accumulate_grouped):
-    // group starts relative to the batch's first rotated item, and head flags;
-    // host arrays stay alive (and distinct per batch) for the async copies
+    // group starts relative to the run's first rotated item, and head flags;
+    // host arrays stay alive (and distinct per run) for the async copies
     static const bool no_group = getenv("HS_NO_GROUP_ROT") != nullptr;   // A/B knob
     std::vector<int> hGS(2 * P + 2);
     std::vector<unsigned char> hHead(P);
@@ -573,27 +617,6 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs,
         set_error("out of device memory (group tables)");
         return (hs_status)HS_OUT_OF_MEMORY;
     }
-    // batches: up to B pairs and at most max_gen distinct non-resident keys
-    std::vector<int64_t> bstart;
-    std::vector<std::vector<u32>> bsteps_all;
-    for (int64_t s = 0, bnext; s < P; s = bnext) {
-        std::vector<u32> bsteps;
-        int64_t ngen = 0;
-        bnext = s;
-        while (bnext < P && bnext - s < B) {
-            const u32 r = hR[bnext];
-            if (r && (bsteps.empty() || bsteps.back() != r)) {
-                const bool lazy = !KP.resident(r);
-                if (lazy && ngen + 1 > max_gen && bnext > s) break;
-                bsteps.push_back(r);
-                ngen += lazy;
-            }
-            bnext++;
-        }
-        bstart.push_back(s);
-        bsteps_all.push_back(bsteps);
-    }
-    bstart.push_back(P);
     for (size_t bi = 0; bi + 1 < bstart.size(); bi++) {
         const int64_t s = bstart[bi], bnext = bstart[bi + 1];
         const std::vector<u32>& bsteps = bsteps_all[bi];
@@ -605,13 +628,12 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs,
             ks_ = KP.prefetch(bsteps_all[bi + 1], bsteps);
             if (ks_ != HS_OK) return ks_;
         }
-        for (int64_t t = s, k = -1; t < bnext; t++) {
-            if (hR[t] && (k < 0 || bsteps[k] != hR[t])) k++;
-            hK[t] = hR[t] ? bkeys[k] : nullptr;
+        {
+            std::unordered_map<u32, const u64*> kmap;
+            for (size_t k = 0; k < bsteps.size(); k++) kmap[bsteps[k]] = bkeys[k];
+            for (int64_t t = s; t < bnext; t++) hK[t] = hR[t] ? kmap[hR[t]] : nullptr;
         }
         HS_CUDA(cudaMemcpyAsync(dK + s, hK.data() + s, bn * sizeof(u64*), cudaMemcpyHostToDevice, st));
-        int z = 0;
-        while (z < bn && hG[s + z] == 0) z++;
         // mult_ct + relinearize, level L, then rescale L -> L-1 fused with the
         // mask product (mask in Montgomery form)
         static const bool split_mdr = getenv("HS_SPLIT_MODDOWN_RESCALE") != nullptr;
@@ -630,36 +652,49 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs,
         // rescale L-1 -> L-2
         rescale_batch(d, bn, L - 1, 2, strided(Mb, (size_t)2 * L * n), strided(Cb, ctL2),
                       ItemPtr{nullptr, nullptr, 0}, Tb, st);
-        // accumulation rotations (step-0 pairs form the sorted prefix)
-        accumulate(d, z, L - 1, 2, strided(Cb, ctL2), out, st);
+        // accumulation per output run of the batch (one run without tiling);
+        // step-0 pairs form each run's sorted prefix
         static const bool split_rot = getenv("HS_SPLIT_ROTATE_ACCUM") != nullptr;
-        bool done = false;
-        const int nr = bn - z;
-        if (nr > 0 && !split_rot && !no_group && (int)bsteps.size() < nr) {
-            // runs of equal steps among the rotated items [s+z, bnext)
-            int* gsh = hGS.data() + (s + z) + bi;              // distinct slice per batch
-            int G = 0;
-            for (int t = 0, run = 0; t < nr; t++) {
-                // at most 16 items per group: the group's digit sums stay exact in int64
-                const bool h = t == 0 || hR[s + z + t] != hR[s + z + t - 1] || run == 16;
-                run = h ? 1 : run + 1;
-                hHead[s + z + t] = h;
-                if (h) gsh[G++] = t;
+        for (int64_t r0 = s; r0 < bnext;) {
+            int64_t r1 = r0 + 1;
+            while (r1 < bnext && hO[r1] == hO[r0]) r1++;
+            u64* out = outs[hO[r0]];
+            const int rb = (int)(r0 - s), rn = (int)(r1 - r0);
+            int z = 0;
+            while (z < rn && hG[r0 + z] == 0) z++;
+            accumulate(d, z, L - 1, 2, strided(Cb + (size_t)rb * ctL2, ctL2), out, st);
+            bool done = false;
+            const int nr = rn - z;
+            const int64_t q0 = r0 + z;                     // first rotated item of the run
+            int nsteps_run = 0;
+            for (int64_t t = q0; t < r1; t++) nsteps_run += (t == q0 || hR[t] != hR[t - 1]);
+            if (nr > 0 && !split_rot && !no_group && nsteps_run < nr) {
+                // runs of equal steps among the rotated items [q0, r1)
+                int* gsh = hGS.data() + q0 + bi;           // distinct slice per run
+                int G = 0;
+                for (int t = 0, run = 0; t < nr; t++) {
+                    // at most 16 items per group: the group's digit sums stay exact in int64
+                    const bool h = t == 0 || hR[q0 + t] != hR[q0 + t - 1] || run == 16;
+                    run = h ? 1 : run + 1;
+                    hHead[q0 + t] = h;
+                    if (h) gsh[G++] = t;
+                }
+                gsh[G] = nr;
+                int* dgs = dGS + (gsh - hGS.data());
+                HS_CUDA(cudaMemcpyAsync(dgs, gsh, (G + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
+                HS_CUDA(cudaMemcpyAsync(dHead + q0, hHead.data() + q0, nr, cudaMemcpyHostToDevice, st));
+                done = rotate_accumulate_grouped(d, nr, G, dgs, dHead + q0, L - 2,
+                                                 strided(Cb + (size_t)(rb + z) * ctL2, ctL2), dG + q0, dK + q0,
+                                                 out, ks, st);
             }
-            gsh[G] = nr;
-            int* dgs = dGS + (gsh - hGS.data());
-            HS_CUDA(cudaMemcpyAsync(dgs, gsh, (G + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
-            HS_CUDA(cudaMemcpyAsync(dHead + s + z, hHead.data() + s + z, nr, cudaMemcpyHostToDevice, st));
-            done = rotate_accumulate_grouped(d, nr, G, dgs, dHead + s + z, L - 2,
-                                             strided(Cb + (size_t)z * ctL2, ctL2), dG + s + z, dK + s + z, out,
-                                             ks, st);
-        }
-        if (nr > 0 && !done && (split_rot || !rotate_accumulate(d, nr, L - 2, strided(Cb + (size_t)z * ctL2, ctL2),
-                                                                 dG + s + z, dK + s + z, out, ks, st,
-                                                                 (int)bsteps.size()))) {
-            rotate_batch(d, bn - z, L - 2, strided(Cb + (size_t)z * ctL2, ctL2), dG + s + z, dK + s + z,
-                         strided(Fb + (size_t)z * ctL2, ctL2), ks, st);
-            accumulate(d, bn - z, L - 1, 2, strided(Fb + (size_t)z * ctL2, ctL2), out, st);
+            if (nr > 0 && !done &&
+                (split_rot || !rotate_accumulate(d, nr, L - 2, strided(Cb + (size_t)(rb + z) * ctL2, ctL2),
+                                                 dG + q0, dK + q0, out, ks, st, nsteps_run))) {
+                rotate_batch(d, nr, L - 2, strided(Cb + (size_t)(rb + z) * ctL2, ctL2), dG + q0, dK + q0,
+                             strided(Fb + (size_t)(rb + z) * ctL2, ctL2), ks, st);
+                accumulate(d, nr, L - 1, 2, strided(Fb + (size_t)(rb + z) * ctL2, ctL2), out, st);
+            }
+            r0 = r1;
         }
         KP.release(bsteps);
     }
@@ -713,8 +748,8 @@ hs_status hs_spmspm_csr_csc(hs_ctx* c, int32_t dim, const int64_t* oa, const int
     const auto t0 = std::chrono::steady_clock::now();
     std::vector<PlanPair> pairs;
     merge_pairs(dim, oa, ia, ob, ib, [&](const PlanPair& p) { pairs.push_back(p); });
-    return run_pairs(c, dim, pairs, {ct_a}, {ct_b}, masks, nmasks, out, counters, shard, nshard,
-                     (cudaStream_t)stream, t0);
+    return run_pairs(c, dim, pairs, {ct_a}, {ct_b}, masks, nmasks, std::vector<u64*>{out}, counters, shard,
+                     nshard, (cudaStream_t)stream, t0);
 }
 
 hs_status hs_spmspm_pairs(hs_ctx* c, int32_t dim, const int64_t* pl, int64_t np, const uint64_t* ct_a,
@@ -724,25 +759,26 @@ hs_status hs_spmspm_pairs(hs_ctx* c, int32_t dim, const int64_t* pl, int64_t np,
     const auto t0 = std::chrono::steady_clock::now();
     std::vector<PlanPair> pairs(np);
     for (int64_t p = 0; p < np; p++) pairs[p] = PlanPair{pl[4 * p], pl[4 * p + 1], pl[4 * p + 2], pl[4 * p + 3]};
-    return run_pairs(c, dim, pairs, {ct_a}, {ct_b}, masks, nmasks, out, counters, shard, nshard,
-                     (cudaStream_t)stream, t0);
+    return run_pairs(c, dim, pairs, {ct_a}, {ct_b}, masks, nmasks, std::vector<u64*>{out}, counters, shard,
+                     nshard, (cudaStream_t)stream, t0);
 }
 
 hs_status hs_spmspm_multi(hs_ctx* c, int32_t dim, const int64_t* pl, int64_t np, const uint64_t* const* cts_a,
                           const uint64_t* const* cts_b, int32_t nprod, const uint64_t* const* masks,
-                          int64_t nmasks, uint64_t* out, hs_counters* counters, int32_t shard, int32_t nshard,
-                          void* stream) {
+                          int64_t nmasks, uint64_t* const* outs, int32_t nout, hs_counters* counters,
+                          int32_t shard, int32_t nshard, void* stream) {
     const auto t0 = std::chrono::steady_clock::now();
-    if (nprod < 1) {
-        set_error("hs_spmspm_multi: no operand products");
+    if (nprod < 1 || nout < 1) {
+        set_error("hs_spmspm_multi: no operand products or outputs");
         return (hs_status)HS_PARAMETER_ERROR;
     }
     std::vector<PlanPair> pairs(np);
     for (int64_t p = 0; p < np; p++)
-        pairs[p] = PlanPair{pl[5 * p], pl[5 * p + 1], pl[5 * p + 2], pl[5 * p + 3], (int32_t)pl[5 * p + 4]};
+        pairs[p] = PlanPair{pl[6 * p], pl[6 * p + 1], pl[6 * p + 2], pl[6 * p + 3], (int32_t)pl[6 * p + 4],
+                            (int32_t)pl[6 * p + 5]};
     return run_pairs(c, dim, pairs, std::vector<const u64*>(cts_a, cts_a + nprod),
-                     std::vector<const u64*>(cts_b, cts_b + nprod), masks, nmasks, out, counters, shard, nshard,
-                     (cudaStream_t)stream, t0);
+                     std::vector<const u64*>(cts_b, cts_b + nprod), masks, nmasks,
+                     std::vector<u64*>(outs, outs + nout), counters, shard, nshard, (cudaStream_t)stream, t0);
 }
 
 hs_status hs_reduce_mod(hs_ctx* c, uint64_t* data, int32_t npoly, int32_t nlimbs, void* stream) {

@@ -199,22 +199,31 @@ def run_pairs(enc_a: EncryptedSparseMatrix, enc_b: EncryptedSparseMatrix, ctx, k
                            dim=dim)
 
 
-def run_products(products, ctx, keys, counter: OpCounter, mask_cache: MaskCache | None,
-                 shard: tuple = (0, 1)) -> EncryptedResult:
-    """Several CSR x CSC products summed into ONE output ciphertext in one
-    runner call (hs_spmspm_multi): the output block C[I][J] = sum_K
-    A[I][K] B[K][J] of the tiled product.  Pairs of all products are scheduled
-    together, so each Galois key is generated once per step for the block.
-    Bit-identical to running the products one by one and joining them with
-    eval_add (a modular sum); the logical counters are the same as well."""
-    prods = []
-    for ea, eb in products:
-        p = plan_csr_csc(ea.meta, eb.meta)
-        if len(p):
-            prods.append((ea, eb, p))
-    dim = products[0][0].dim if products else 0
+def run_blocks(blocks: dict, ctx, keys, counter: OpCounter, mask_cache: MaskCache | None,
+               shard: tuple = (0, 1)) -> dict:
+    """Output blocks of a tiled product, ``{key: [(enc_a, enc_b), ...]}``
+    (C[I][J] = sum_K A[I][K] B[K][J]), in ONE runner call (hs_spmspm_multi):
+    the pairs of every product and block are scheduled together, sorted by
+    accumulation step, so each Galois key is generated once for the whole
+    product and each (operand, step) alignment is rotated once.  Every
+    block's result is bit-identical to running its products one by one and
+    joining them with eval_add (a modular sum), and the logical counters are
+    the same as well.  Returns ``{key: EncryptedResult}``."""
+    keys_order = sorted(blocks)
+    prods, rows = [], []
+    dim = 0
+    for o, key in enumerate(keys_order):
+        for ea, eb in blocks[key]:
+            dim = ea.dim
+            p = plan_csr_csc(ea.meta, eb.meta)
+            if len(p):
+                k = len(prods)
+                prods.append((ea, eb, o))
+                rows.append(np.concatenate([p, np.full((len(p), 1), k, dtype=np.int64),
+                                            np.full((len(p), 1), o, dtype=np.int64)], axis=1))
+    out = {key: EncryptedResult(ctxt=None, dim=dim) for key in keys_order}
     if not prods:
-        return EncryptedResult(ctxt=None, dim=dim)
+        return out
     params = ctx.params
     L = params.levels
     if mask_cache is None:
@@ -223,32 +232,31 @@ def run_products(products, ctx, keys, counter: OpCounter, mask_cache: MaskCache 
         from .errors import KeyMissingError
         raise KeyMissingError("no relinearization key in bundle")
     start = time.perf_counter()
-    scale = None
-    cta, ctb, rows = [], [], []
-    for k, (ea, eb, p) in enumerate(prods):
+    scale = {}
+    for ea, eb, o in prods:
         ca, cb = ea.ctxt, eb.ctxt
         if ca.level != L or cb.level != L:
             raise EvalError(f"level mismatch: {ca.level}/{cb.level} != {L}")
         if ca.degree != 1 or cb.degree != 1:
             raise EvalError("eval_mult_ct expects degree-1 ciphertexts")
         s_k = _result_scale(ctx, ca.scale, cb.scale)
-        if scale is None:
-            scale = s_k
-        elif abs(s_k - scale) > 1e-9 * max(abs(scale), abs(s_k)):
+        if o not in scale:
+            scale[o] = s_k
+        elif abs(s_k - scale[o]) > 1e-9 * max(abs(scale[o]), abs(s_k)):
             raise EvalError("scale mismatch between block products")   # eval_add's check
-        cta.append(ca.data)
-        ctb.append(cb.data)
-        rows.append(np.concatenate([p, np.full((len(p), 1), k, dtype=np.int64)], axis=1))
     pl = np.ascontiguousarray(np.concatenate(rows), dtype=np.int64)
-    out = D.empty((2, L - 1, params.ring_degree))
+    outs = [D.empty((2, L - 1, params.ring_degree)) for _ in keys_order]
     cnt = HsCounters()
+    cta = [ea.ctxt.data for ea, _, _ in prods]
+    ctb = [eb.ctxt.data for _, eb, _ in prods]
     pa = (ctypes.c_void_p * len(prods))(*[D.ptr(t) for t in cta])
     pb = (ctypes.c_void_p * len(prods))(*[D.ptr(t) for t in ctb])
+    po = (ctypes.c_void_p * len(outs))(*[D.ptr(t) for t in outs])
     for attempt in range(2):
         mt, nm = mask_cache.table()
-        st = lib().hs_spmspm_multi(ctx.handle, dim, pl.ctypes.data_as(c_i64p), len(pl), pa, pb,
-                                   len(prods), mt, nm, D.ptr(out), ctypes.byref(cnt), shard[0],
-                                   shard[1], D.stream())
+        st = lib().hs_spmspm_multi(ctx.handle, dim, pl.ctypes.data_as(c_i64p), len(pl), pa, pb, len(prods),
+                                   mt, nm, po, len(outs), ctypes.byref(cnt), shard[0], shard[1],
+                                   D.stream())
         if st == 4 and attempt == 0 and "not prewarmed" in lib().hs_last_error().decode():
             for pos in np.unique(np.minimum(pl[:, 2], pl[:, 3])):
                 mask_cache.get(int(pos))
@@ -259,7 +267,16 @@ def run_products(products, ctx, keys, counter: OpCounter, mask_cache: MaskCache 
     _counter_update(counter, cnt)
     ctx.relin_noops += cnt.relin_noops
     counter.wall_time += time.perf_counter() - start
-    return EncryptedResult(ctxt=Ciphertext(out, scale, L - 2), dim=dim)
+    for o, key in enumerate(keys_order):
+        if o in scale:
+            out[key] = EncryptedResult(ctxt=Ciphertext(outs[o], scale[o], L - 2), dim=dim)
+    return out
+
+
+def run_products(products, ctx, keys, counter: OpCounter, mask_cache: MaskCache | None,
+                 shard: tuple = (0, 1)) -> EncryptedResult:
+    """Several CSR x CSC products summed into ONE output (one block)."""
+    return run_blocks({0: list(products)}, ctx, keys, counter, mask_cache, shard)[0]
 
 
 def _require_layouts(enc_a, enc_b, layout_a: Layout, layout_b: Layout):

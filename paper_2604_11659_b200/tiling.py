@@ -124,15 +124,15 @@ def required_rotation_steps_tiled(ta: TiledMatrix, tb: TiledMatrix) -> set:
 
 def spmm_tiled(ta: TiledMatrix, tb: TiledMatrix, ctx, keys, counter=None, mask_cache=None,
                spmm=None) -> TiledResult:
-    """Block SpMSpM.  Default: one runner call per output block C[I][J]
-    over all its products A[I][K] x B[K][J] (engine.run_products:
-    hs_spmspm_multi schedules their pairs together, so a Galois key is
-    generated once per step for the block, and the products' sum is the
-    runner's own modular accumulation).  With ``spmm`` given (e.g. the
+    """Block SpMSpM.  Default: ONE runner call for every output block
+    C[I][J] and all its products A[I][K] x B[K][J] (engine.run_blocks:
+    hs_spmspm_multi schedules all pairs together, so a Galois key is
+    generated once per step for the whole product, and each block's sum is
+    the runner's own modular accumulation).  With ``spmm`` given (e.g. the
     multi-GPU runner), every non-empty product runs on it and the partial
     products of a block are joined with eval_add.  Both are bit-identical,
     with the same logical counters (the joins count as adds)."""
-    from .engine import MaskCache, OpCounter, run_products
+    from .engine import MaskCache, OpCounter, run_blocks
     if ta.layout is not Layout.CSR or tb.layout is not Layout.CSC:
         raise ParameterError("tiled product needs CSR x CSC operands")
     counter = counter if counter is not None else OpCounter()
@@ -142,8 +142,7 @@ def spmm_tiled(ta: TiledMatrix, tb: TiledMatrix, ctx, keys, counter=None, mask_c
         blocks: dict = {}
         for I, K, J in block_products(ta, tb):
             blocks.setdefault((I, J), []).append((ta.tiles[(I, K)], tb.tiles[(K, J)]))
-        for key in sorted(blocks):
-            part = run_products(blocks[key], ctx, keys, counter, mask_cache)
+        for key, part in run_blocks(blocks, ctx, keys, counter, mask_cache).items():
             if part.ctxt is not None:
                 res.tiles[key] = part
         return res
