@@ -592,6 +592,7 @@ def run_b200_arm(args, wl):
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "result_repeatable": same,
+            "pair_ranges": int(c.ranges),
             "accuracy": {"frobenius_vs_plaintext": frob, "tolerance": 1e-6, "ok": frob < 1e-6,
                          "note": "decrypted result of the first execution vs plain_matmul "
                                  "(the reference's acceptance bound, tests/test_acceptance.py:30-31)"},

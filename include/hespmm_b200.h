@@ -52,6 +52,7 @@ typedef struct {
     int64_t physical_alignment;    /* distinct (operand, step) rotations executed */
     int64_t has_result;            /* 0 when the schedule is empty (engine.py:162-164) */
     double plan_ms;                /* host planning time inside the call */
+    int64_t ranges;                /* pair ranges run (> 1 when the aligned operands exceed HBM) */
 } hs_counters;
 
 const char* hs_last_error(void);

@@ -27,7 +27,7 @@ class HsCounters(ctypes.Structure):
     _fields_ = [(name, ctypes.c_int64) for name in (
         "ct_ct_mults", "pt_mults", "rotations", "relins", "relin_noops", "rescales", "adds",
         "alignment_rotations", "accumulation_rotations", "pairs", "physical_alignment",
-        "has_result")] + [("plan_ms", ctypes.c_double)]
+        "has_result")] + [("plan_ms", ctypes.c_double), ("ranges", ctypes.c_int64)]
 
 
 # name -> (restype, argtypes)

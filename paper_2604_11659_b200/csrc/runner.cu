@@ -438,6 +438,16 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs,
     {
         size_t free_b = 0, total_b = 0;
         if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+            // memory the stream-ordered pool holds but does not use (freed by
+            // the previous call's DeviceArena) is available to this one
+            int dev = 0;
+            cudaMemPool_t mpool;
+            unsigned long long reserved = 0, used = 0;
+            if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&mpool, dev) == cudaSuccess &&
+                cudaMemPoolGetAttribute(mpool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
+                cudaMemPoolGetAttribute(mpool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess &&
+                reserved > used)
+                free_b += (size_t)(reserved - used);
             const size_t pool = c->kpool_buf.size() >= (size_t)(2 * max_gen) ? 0
                               : (size_t)(2 * max_gen) * c->key_bytes();
             const size_t reserve = 2 * budget + pool + ((size_t)2 << 30);
@@ -702,6 +712,7 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs,
     return (hs_status)HS_OK;
     };
 
+    C.ranges = (int64_t)cuts.size() - 1;
     for (size_t ci = 0; ci + 1 < cuts.size(); ci++) {
         hs_status s_ = run_range(cuts[ci], cuts[ci + 1]);
         if (s_ != HS_OK) return s_;

@@ -53,6 +53,7 @@ class OpCounter:
     wall_time: float = 0.0
     physical_alignment: int = 0
     plan_ms: float = 0.0
+    ranges: int = 0                 # most pair ranges one call needed (aligned operands vs HBM)
 
     def as_dict(self) -> dict:
         return {"ct_ct_mults": self.ct_ct_mults, "pt_mults": self.pt_mults,
@@ -125,6 +126,7 @@ def _counter_update(counter: OpCounter, c: HsCounters) -> None:
                  "adds", "alignment_rotations", "accumulation_rotations", "physical_alignment"):
         setattr(counter, name, getattr(counter, name) + getattr(c, name))
     counter.plan_ms += c.plan_ms
+    counter.ranges = max(counter.ranges, int(c.ranges))
 
 
 def _result_scale(ctx, sa: float, sb: float) -> float:
