@@ -447,7 +447,9 @@ def run_b200_arm(args, wl):
         c = engine.OpCounter()
         spmm = hdist.spmm_csr_csc_distributed if world > 1 else engine.spmm_csr_csc
         if tiled:
-            return tiling.spmm_tiled(ea_, eb_, ctx, keys, c, mc, spmm=spmm), c
+            # one GPU: the whole tiled product in one runner call (run_blocks);
+            # several: every block product pair-sharded across the ranks
+            return tiling.spmm_tiled(ea_, eb_, ctx, keys, c, mc, spmm=spmm if world > 1 else None), c
         return spmm(ea_, eb_, ctx, keys, c, mc), c
 
     def result_host(r):
