@@ -595,9 +595,13 @@ def run_b200_arm(args, wl):
             "clocks": clk.summary(),
             "result_repeatable": same,
             "pair_ranges": int(c.ranges),
-            "accuracy": {"frobenius_vs_plaintext": frob, "tolerance": 1e-6, "ok": frob < 1e-6,
-                         "note": "decrypted result of the first execution vs plain_matmul "
-                                 "(the reference's acceptance bound, tests/test_acceptance.py:30-31)"},
+            "accuracy": {"frobenius_vs_plaintext": frob, "reference_bound": 1e-6,
+                         "within_reference_bound": frob < 1e-6,
+                         "note": "decrypted result of the first execution vs the plaintext matmul; "
+                                 "the reference's acceptance bound (tests/test_acceptance.py:30-31) is "
+                                 "for its own sizes -- the CKKS error grows ~ 2^-scale_bits * "
+                                 "sqrt(N^2 * pairs) (SURVEY 8d), so Delta = 2^50 is tight at configs[2] "
+                                 "and exceeds it at the configs[3] size"},
         }
         print(json.dumps(line), flush=True)
     if world > 1:
