@@ -340,6 +340,25 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs,
         set_error("no relinearization key in bundle");
         return (hs_status)HS_KEY_MISSING;
     }
+    // operand ids for the alignment deduplication: ct_a 0, ct_b 1 for one
+    // product (the ids hs_align_provide uses); with several products the
+    // distinct ciphertexts (A[I][K] serves every J), so a block operand is
+    // rotated by a step once for the whole tiled product
+    std::vector<const u64*> operands;
+    std::vector<int> opid_a(cta.size()), opid_b(cta.size());
+    {
+        auto id_of = [&](const u64* ptr) {
+            if (cta.size() > 1)
+                for (size_t k = 0; k < operands.size(); k++)
+                    if (operands[k] == ptr) return (int)k;
+            operands.push_back(ptr);
+            return (int)operands.size() - 1;
+        };
+        for (size_t k = 0; k < cta.size(); k++) {
+            opid_a[k] = id_of(cta[k]);
+            opid_b[k] = id_of(ctb[k]);
+        }
+    }
     for (int64_t p = 0; p < np; p++) {
         const PlanPair& q = pairs[p];
         if (q.k < 0 || q.k >= (int32_t)cta.size() || q.o < 0 || q.o >= (int32_t)outs.size()) {
@@ -350,7 +369,8 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs,
         ia[p] = 0;
         ib[p] = 1;
         if (q.ap != q.bp) {
-            const int src = (q.ap < q.bp ? 1 : 0) + 2 * q.k;  // the higher-positioned operand rotates
+            const bool rot_b = q.ap < q.bp;                   // the higher-positioned operand rotates
+            const int src = rot_b ? opid_b[q.k] : opid_a[q.k];
             const int64_t raw = q.ap < q.bp ? q.bp - q.ap : q.ap - q.bp;
             const u32 r = norm_step(raw, slots);
             C.rotations++;
@@ -367,7 +387,7 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs,
                 } else {
                     idx = it->second;
                 }
-                ((src & 1) ? ib[p] : ia[p]) = idx;
+                (rot_b ? ib[p] : ia[p]) = idx;
             }
             mn = std::min(q.ap, q.bp);
         } else {
@@ -535,11 +555,6 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs,
         if (ks_ != HS_OK) return ks_;
     }
     {
-        std::vector<const u64*> operands;
-        for (size_t k = 0; k < cta.size(); k++) {
-            operands.push_back(cta[k]);
-            operands.push_back(ctb[k]);
-        }
         hs_status s_ = compute_alignments(c, operands, todo, todo_out, KP, A, budget, max_gen, st);
         if (s_ != HS_OK) return s_;
     }
