@@ -470,7 +470,7 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs,
                 free_b += (size_t)(reserved - used);
             const size_t pool = c->kpool_buf.size() >= (size_t)(2 * max_gen) ? 0
                               : (size_t)(2 * max_gen) * c->key_bytes();
-            const size_t reserve = 2 * budget + pool + ((size_t)2 << 30);
+            const size_t reserve = budget + budget / 4 + pool + ((size_t)2 << 30);
             amax = free_b > reserve ? (int64_t)((free_b - reserve) / (ctL * sizeof(u64))) : 1;
             amax = std::max<int64_t>(1, amax);
         }
@@ -555,7 +555,10 @@ hs_status run_pairs(hs_ctx* c, int dim, const std::vector<PlanPair>& pairs,
         if (ks_ != HS_OK) return ks_;
     }
     {
-        hs_status s_ = compute_alignments(c, operands, todo, todo_out, KP, A, budget, max_gen, st);
+        // the alignment scratch lives in its own arena, released before the
+        // pair batches allocate theirs (stream-ordered frees)
+        DeviceArena A1{st};
+        hs_status s_ = compute_alignments(c, operands, todo, todo_out, KP, A1, budget, max_gen, st);
         if (s_ != HS_OK) return s_;
     }
 
