@@ -435,7 +435,7 @@ void or_eval_rotate(const or_ctx *c, const u64 *ct, unsigned r, const u64 *gk, u
     or_perm_tables(n, g, src, neg);
     u64 *tmp = malloc((size_t)n * sizeof(u64));
     u64 *new0 = malloc((size_t)nl * n * sizeof(u64));
-    u64 *digits = malloc((size_t)nl * n * sizeof(u64));
+    u64 *digits = calloc((size_t)nl * n, sizeof(u64));      /* filled below (calloc: no -Wmaybe-uninitialized) */
     u64 *kb = malloc((size_t)nl * n * sizeof(u64));
     for (unsigned i = 0; i < nl; i++) {
         u64 q = c->primes[i];
