@@ -4,6 +4,7 @@
 // in the sm_100a kernels of ops.cu / ntt.cuh.
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -158,11 +159,20 @@ hs_status hs_ctx_create(hs_ctx** out, int device, uint32_t n, uint32_t levels,
     }
     // per-prime constants and twiddles
     std::vector<ulonglong2> tw((size_t)P * n), itw((size_t)P * n);
+    std::vector<double2> twd((size_t)P * n);
     std::vector<u64> pw(n), ipw(n);
     c->pc.resize(P);
+    // Forward NTT butterflies on the FP64 pipe for primes <= 2^50 + 2^40 (every
+    // scaling prime of a scale_bits <= 50 chain; ntt.cuh unit_butterflies_f64
+    // states the bounds).  HS_NTT_F64=0 keeps every prime on the integer path.
+    const char* f64env = getenv("HS_NTT_F64");
+    // (the A/B-only fused ModUp + inner-product kernel finishes integer-path
+    // forward NTTs itself, so it keeps every prime on the integer path)
+    const bool f64_on = !(f64env && f64env[0] == '0') && !getenv("HS_MODUP_FUSED");
     for (int p = 0; p < P; p++) {
         u64 q = c->primes[p];
         c->pc[p] = make_prime_const(q, n);
+        if (f64_on && q <= (1ull << 50) + (1ull << 40)) c->pc[p].pad |= PC_F64;
         u64 psi = find_psi(q, n);
         if (!psi) {
             set_error("no primitive 2n-th root for prime " + std::to_string(q));
@@ -178,6 +188,8 @@ hs_status hs_ctx_create(hs_ctx** out, int device, uint32_t n, uint32_t levels,
         for (u32 i = 0; i < n; i++) {
             u32 r = brev(i, c->log_n);
             tw[(size_t)p * n + i] = shoup_pair(pw[r], q);
+            // w < 2^51 is exact in a double; RN(w / q) by one IEEE division of exact operands
+            twd[(size_t)p * n + i] = make_double2((double)pw[r], (double)pw[r] / (double)q);
             itw[(size_t)p * n + i] = shoup_pair(ipw[r], q);
         }
     }
@@ -211,7 +223,9 @@ hs_status hs_ctx_create(hs_ctx** out, int device, uint32_t n, uint32_t levels,
     size_t off_df = off_itw + itw.size() * sizeof(ulonglong2);
     size_t off_ai = off_df + df.size() * sizeof(ulonglong2);
     size_t off_ql = off_ai + auxinv.size() * sizeof(ulonglong2);
-    size_t total = off_ql + qlinv.size() * sizeof(ulonglong2);
+    size_t off_twd = off_ql + qlinv.size() * sizeof(ulonglong2);
+    off_twd = (off_twd + 255) & ~(size_t)255;
+    size_t total = off_twd + twd.size() * sizeof(double2);
     cudaError_t e = cudaMalloc(&c->d_blob, total);
     if (e != cudaSuccess) {
         set_error(std::string("cudaMalloc tables: ") + cudaGetErrorString(e));
@@ -224,7 +238,8 @@ hs_status hs_ctx_create(hs_ctx** out, int device, uint32_t n, uint32_t levels,
     cudaMemcpy(base + off_itw, itw.data(), itw.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice);
     cudaMemcpy(base + off_df, df.data(), df.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice);
     cudaMemcpy(base + off_ai, auxinv.data(), auxinv.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice);
-    e = cudaMemcpy(base + off_ql, qlinv.data(), qlinv.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice);
+    cudaMemcpy(base + off_ql, qlinv.data(), qlinv.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice);
+    e = cudaMemcpy(base + off_twd, twd.data(), twd.size() * sizeof(double2), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
         set_error(std::string("table upload: ") + cudaGetErrorString(e));
         cudaFree(c->d_blob);
@@ -243,6 +258,7 @@ hs_status hs_ctx_create(hs_ctx** out, int device, uint32_t n, uint32_t levels,
     d.dfR = d.df + (L + 1);
     d.auxinv = (const ulonglong2*)(base + off_ai);
     d.qlinv = (const ulonglong2*)(base + off_ql);
+    d.twd = (const double2*)(base + off_twd);
     *out = c;
     return (hs_status)HS_OK;
 }

@@ -25,8 +25,9 @@ struct PrimeConst {
     u64 m64;         // floor(2^64 / q): generic 64-bit Barrett (reduce64)
     u64 r_sh;        // floor(r_mod 2^64 / q): Shoup companion of 2^64 mod q
     u32 k;           // bitlen(q)
-    u32 pad;
+    u32 pad;         // flags: PC_F64 = forward NTT butterflies on the FP64 pipe (q <= 2^50 + 2^40)
 };
+#define PC_F64 1u
 
 HS_DEV u64 mulhi64(u64 a, u64 b) { return __umul64hi(a, b); }
 

@@ -323,6 +323,73 @@ HS_DEV void unit_butterflies(u64* v, const ulonglong2* __restrict__ tw, u32 Y, u
     }
 }
 
+// ---- forward butterflies on the FP64 pipe (primes q <= 2^50 + 2^40, PC_F64)
+// The Shoup products above are 64-bit multiplies (IMAD.WIDE / IMAD.HI) that
+// keep the FMA-heavy pipe ~80% busy; B200 also has a full-rate FP64 pipe, and
+// for ~50-bit primes a residue is an exact double.  Values are signed
+// integers held in doubles; every operation below is exact:
+//   rint(y), |y| < 2^51:   FMA against 1.5*2^52 then subtract it (the sum stays
+//                          in [2^52, 2^53), where the spacing of doubles is 1)
+//   t = a*w mod q (lazy):  hi = RN(a w), lo = a w - hi (FMA, exact: TwoProduct),
+//                          Q = rint(a * RN(w/q)), t = (hi - Q q) + lo (FMA then
+//                          add; both results are integers below 2^53, hence
+//                          exact), so t = a w - Q q.
+//   |Q - a w/q| <= 1/2 + |a| 2^-53  =>  |t| <= (1/2 + k |a|/q) q, k = q 2^-53.
+// Bounds (k <= 0.1252): the first pass reduces its inputs to |x| <= q/2; the
+// unmultiplied input x is reduced to |x| <= q/2 at every odd global stage, so
+// after a reducing stage B_r = 1 + k B_f and after a free one B_f = B_r + 1/2
+// + k B_r (in units of q): the fixed point B_f = 1.89q bounds every value,
+// and every multiplied |a| < 1.89q (1 + 2^-10) 2^50 < 2^51 keeps rint exact.
+// The last pass reduces to [-q/2, q/2] and returns [q/2, 3q/2] as u64.
+// Passes hand raw doubles to each other.  Any other prime (the 60-bit first
+// and auxiliary primes) stays on the integer path.
+HS_DEV constexpr bool f64_reduce_at(int gs) { return gs & 1; }
+constexpr double kF64Magic = 6755399441055744.0;   // 1.5 * 2^52
+
+HS_DEV double f64_rint_mul(double a, double b) {
+    return __dsub_rn(__fma_rn(a, b, kF64Magic), kF64Magic);   // rint(a b), |a b| < 2^51
+}
+HS_DEV double f64_reduce(double x, double q, double qinv) {
+    return __fma_rn(-f64_rint_mul(x, qinv), q, x);             // x - q rint(x / q), |.| <= q/2 + tiny
+}
+HS_DEV double f64_mulmod(double a, double w, double wq, double q) {
+    const double hi = __dmul_rn(a, w);
+    const double lo = __fma_rn(a, w, -hi);
+    const double Q = f64_rint_mul(a, wq);
+    return __dadd_rn(__fma_rn(-Q, q, hi), lo);
+}
+
+template <int R, int GS>
+HS_DEV void unit_butterflies_f64(u64* v, const double2* __restrict__ tw, u32 Y, double q, double qinv) {
+    constexpr int NU = 1 << R;
+#pragma unroll
+    for (int j = 0; j < R; j++) {
+        const double2* __restrict__ twp = tw + (Y << j);
+        const int bit = 1 << (R - 1 - j);
+#pragma unroll
+        for (int e = 0; e < NU; e++) {
+            if (e & bit) continue;
+            const double2 w = twp[e >> (R - j)];
+            double x = __longlong_as_double((long long)v[e]);
+            if (f64_reduce_at(GS + j)) x = f64_reduce(x, q, qinv);
+            const double t = f64_mulmod(__longlong_as_double((long long)v[e + bit]), w.x, w.y, q);
+            v[e] = (u64)__double_as_longlong(__dadd_rn(x, t));
+            v[e + bit] = (u64)__double_as_longlong(__dsub_rn(x, t));
+        }
+    }
+}
+
+// u64 in [0, 4q) -> reduced double bits, |x| <= q/2 (first forward pass)
+HS_DEV u64 f64_enter(u64 u, double q, double qinv) {
+    return (u64)__double_as_longlong(f64_reduce(__ull2double_rn(u), q, qinv));
+}
+// double bits, |x| < 2^52.5 -> u64 in [q/2, 3q/2] (last forward pass):
+// x - q rint(x/q) + q + 2^52 lies in [2^52, 2^53), whose mantissa is the value
+HS_DEV u64 f64_leave(u64 bits, double q, double qinv, double q_plus_2p52) {
+    const double r = __dadd_rn(f64_reduce(__longlong_as_double((long long)bits), q, qinv), q_plus_2p52);
+    return (u64)__double_as_longlong(r) & 0x000FFFFFFFFFFFFFull;
+}
+
 // Job interface: `typename Job::Ctx ctx = job.make(jb)` is evaluated once per
 // CTA (pointer-table lookups, index decoding), then prime(ctx),
 // load(ctx, j, P), scratch(ctx), store(ctx, j, v, P) per element.  load()
@@ -375,8 +442,11 @@ struct PassEngine {
         typename Job::Ctx jc;
         PrimeConst P;
         const ulonglong2* __restrict__ tw;
+        const double2* __restrict__ twd;   // FP64 forward roots (f64)
         u32 t, hi0, lo0;
         u64 nq, four_q;
+        bool f64;                          // forward pass on the FP64 pipe (PC_F64)
+        double qd, qinvd;
         HS_DEV u32 gidx(u32 h, u32 g, u32 c) const {
             return ((hi0 + h) << (LOGN - S0)) | (g << LO_BITS) | (lo0 + c);
         }
@@ -427,7 +497,10 @@ struct PassEngine {
             for (int k = 0; k < 2; k++) {
                 const auto u = M::unit(E.t + k * T);
                 const u32 Y = (((1u << S0) + E.hi0 + u.h) << M::AA) + u.gh;
-                unit_butterflies<FWD, M::RR, S0 + M::AA>(v, E.tw, Y, E.nq, E.P.two_q, E.four_q);
+                if (FWD && E.f64)
+                    unit_butterflies_f64<M::RR, S0 + M::AA>(v, E.twd, Y, E.qd, E.qinvd);
+                else
+                    unit_butterflies<FWD, M::RR, S0 + M::AA>(v, E.tw, Y, E.nq, E.P.two_q, E.four_q);
 #pragma unroll
                 for (int e = 0; e < M::NU; e++) {
                     const u64 x = v[e];
@@ -440,7 +513,29 @@ struct PassEngine {
             for (int k = 0; k < M::UPT; k++) {
                 const auto u = M::unit(E.t + k * T);
                 const u32 Y = (((1u << S0) + E.hi0 + u.h) << M::AA) + u.gh;
-                unit_butterflies<FWD, M::RR, S0 + M::AA>(v + k * M::NU, E.tw, Y, E.nq, E.P.two_q, E.four_q);
+                if (FWD && E.f64)
+                    unit_butterflies_f64<M::RR, S0 + M::AA>(v + k * M::NU, E.twd, Y, E.qd, E.qinvd);
+                else
+                    unit_butterflies<FWD, M::RR, S0 + M::AA>(v + k * M::NU, E.tw, Y, E.nq, E.P.two_q, E.four_q);
+            }
+        }
+    }
+    // FP64 forward path: enter after the first pass's load, leave before the
+    // last pass's store (passes in between exchange raw doubles)
+    HS_DEV static void f64_in(u64* v, const Env& E) {
+        if constexpr (FWD && FIRST) {
+            if (E.f64) {
+#pragma unroll
+                for (int k = 0; k < EPT; k++) v[k] = f64_enter(v[k], E.qd, E.qinvd);
+            }
+        }
+    }
+    HS_DEV static void f64_out(u64* v, const Env& E) {
+        if constexpr (FWD && LAST) {
+            if (E.f64) {
+                const double k = E.qd + 4503599627370496.0;   // q + 2^52
+#pragma unroll
+                for (int i = 0; i < EPT; i++) v[i] = f64_leave(v[i], E.qd, E.qinvd, k);
             }
         }
     }
@@ -486,8 +581,10 @@ struct PassEngine {
             __syncthreads();
             gather<RFIRST>(buf, v, E);
         }
+        f64_in(v, E);
         compute<RFIRST>(v, E);
         rest<1>(sm, v, E);
+        f64_out(v, E);
         // ---- store
         if constexpr (ML::direct) {
             constexpr u32 gstride = 1u << (ML::LOWB + LO_BITS);
@@ -536,6 +633,12 @@ ntt_pass_kernel(Dev d, Job job, int jbase) {
     E.t = threadIdx.x;
     E.nq = 0ull - E.P.q;
     E.four_q = E.P.two_q << 1;
+    E.f64 = FWD && (E.P.pad & PC_F64);
+    if (FWD) {
+        E.twd = d.twd + ((size_t)p << LOGN);
+        E.qd = (double)E.P.q;
+        E.qinvd = __drcp_rn(E.qd);
+    }
     // One code path for every prime: a lazy forward variant (no upper-input
     // reduction for sub-2^56 primes) saved ~5 instructions per butterfly but
     // doubled the kernel's code, and instruction-cache misses cost more than

@@ -80,6 +80,38 @@ def test_batched_ntt_every_ring_degree(pkg, oracle_mod, log_n):
     del torch
 
 
+def test_ntt_extreme_inputs(pkg, oracle_mod):
+    """Forward/inverse NTT of constant q-1, (q-1)/2, alternating 0/q-1 and
+    one-hot limbs at N=2^16 (FP64-pipe butterflies on the ~50-bit primes,
+    integer ones on the 60-bit primes) vs the oracle: the bound analysis of
+    ntt.cuh unit_butterflies_f64 exercised at its largest magnitudes."""
+    from paper_2604_11659_b200 import device as D
+    from paper_2604_11659_b200._lib import check, lib
+    O = oracle_mod
+    n = 1 << 16
+    params = pkg.build_params(n, 50, 3, 2024)
+    ctx = pkg.CkksContext(params)
+    octx = O.OracleContext(O.build_params(n, 50, 3, 2024))
+    primes = [*params.modulus_chain, params.aux_prime]
+    P = len(primes)
+    pats = []
+    for q in [np.uint64(x) for x in primes]:
+        alt = np.zeros(n, dtype=np.uint64)
+        alt[1::2] = q - np.uint64(1)
+        one = np.zeros(n, dtype=np.uint64)
+        one[n - 1] = q - np.uint64(1)
+        pats.append([np.full(n, q - np.uint64(1)), np.full(n, (q - np.uint64(1)) // np.uint64(2)), alt, one])
+    host = np.stack([np.stack([pats[p][k] for p in range(P)]) for k in range(4)])
+    d = D.to_dev(host)
+    check(lib().hs_ntt(ctx.handle, D.ptr(d), 4, P, 0, 0, D.stream()))
+    fwd = D.to_host(d)
+    for k in range(4):
+        for p in range(P):
+            assert np.array_equal(fwd[k, p], octx.ntt_limb(host[k, p], p)), (k, p)
+    check(lib().hs_ntt(ctx.handle, D.ptr(d), 4, P, 0, 1, D.stream()))
+    assert np.array_equal(D.to_host(d), host)
+
+
 # ------------------------------------------------------- CKKS primitives
 
 def _product_ops_pipeline(P, key):

@@ -8,7 +8,9 @@ process on the same seeded product and must give the same ciphertext bits.
 HS_NO_GROUP_ROT turns off the per-key-group ModUp/inner product of the
 accumulation rotations, HS_KSI_LDG the bulk-async inner-product kernel,
 HS_ALIGN_MAX=3 runs the pair list in ranges of at most 3 aligned operands
-(the path large configs take when the aligned operands exceed HBM).
+(the path large configs take when the aligned operands exceed HBM), and
+HS_NTT_F64=0 keeps every forward NTT on the integer (Shoup) butterflies
+instead of the FP64-pipe butterflies used for ~50-bit primes.
 The default path itself is checked against the oracle and the golden
 vectors in test_gpu_parity.py.
 """
@@ -39,7 +41,8 @@ print("DIGESTS " + json.dumps(out))
 """
 
 SWITCHES = ["HS_SPLIT_MODDOWN_RESCALE", "HS_TOPLIMB_FWD", "HS_SPLIT_ROTATE_ACCUM", "HS_NO_GROUP_ROT",
-            "HS_KSI_LDG", "HS_ALIGN_MAX"]
+            "HS_KSI_LDG", "HS_ALIGN_MAX", "HS_NTT_F64"]
+VALUES = {"HS_ALIGN_MAX": "3", "HS_NTT_F64": "0"}     # 3 aligned operands per range; integer butterflies
 
 
 def _digests(env_on):
@@ -47,7 +50,7 @@ def _digests(env_on):
     for k in SWITCHES:
         env.pop(k, None)
     for k in env_on:
-        env[k] = "3" if k == "HS_ALIGN_MAX" else "1"     # 3 aligned operands per range
+        env[k] = VALUES.get(k, "1")
     p = subprocess.run([sys.executable, "-c", SCRIPT, ROOT, os.path.join(ROOT, "tests")], env=env,
                        capture_output=True, text=True, timeout=900)
     assert p.returncode == 0, p.stderr[-2000:]
@@ -58,5 +61,5 @@ def _digests(env_on):
 def test_merged_sequences_equal_plain_sequences():
     base = _digests([])
     for on in (["HS_SPLIT_MODDOWN_RESCALE"], ["HS_TOPLIMB_FWD"], ["HS_SPLIT_ROTATE_ACCUM"],
-               ["HS_NO_GROUP_ROT"], ["HS_KSI_LDG"], ["HS_ALIGN_MAX"], SWITCHES):
+               ["HS_NO_GROUP_ROT"], ["HS_KSI_LDG"], ["HS_ALIGN_MAX"], ["HS_NTT_F64"], SWITCHES):
         assert _digests(on) == base, on
