@@ -3,7 +3,7 @@
 # (N=2^16, L=24) and of device key generation; run under gpurun (1 GPU).
 # profile_step --no-align 48: only pairs without alignment rotations, so the
 # first ModUp / inner-product launches are a relinearisation pair batch.
-# Usage: tools/ncu_cfg3.sh <tag>
+# Usage: tools/ncu_cfg3.sh <tag> [modup,ks_inner,keyfused,uni_emit]
 set -u
 TAG=${1:-r02}
 OUT=gpurun_out
@@ -20,7 +20,9 @@ cap() {  # name regex skip count
     rm -f "$rep.ncu-rep"
   fi
 }
-cap modup 'JobModUp>' 0 2
-cap ks_inner 'ks_inner_tma' 0 1
-cap keyfused 'JobKeyFused' 0 2
-cap uni_emit 'pk_uni_emit' 0 1
+WHICH=${2:-modup,ks_inner,keyfused,uni_emit}
+[[ $WHICH == *modup* ]] && cap modup 'JobModUp>' 0 2
+[[ $WHICH == *ks_inner* ]] && cap ks_inner 'ks_inner_tma' 0 1
+[[ $WHICH == *keyfused* ]] && cap keyfused 'JobKeyFused' 0 2
+[[ $WHICH == *uni_emit* ]] && cap uni_emit 'pk_uni_emit' 0 1
+true

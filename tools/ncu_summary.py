@@ -10,6 +10,8 @@ KEYS = [
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue%"),
     ("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", "alu%"),
     ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "fma%"),
+    ("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active", "fmaheavy%"),
+    ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "fp64%"),
     ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram%"),
     ("dram__bytes_read.sum", "dram_rd"),
     ("dram__bytes_write.sum", "dram_wr"),
