@@ -31,7 +31,9 @@ Roofline: the key-switch kernels are timed inside the timed steps with CUDA
 events on their own launching stream (hs_probe_*): the ModUp NTT passes and
 the key inner product; the one with the larger share of the step is the
 ``roofline`` entry (HBM GB/s vs MEASURED_PEAKS.json), with its INT-pipe
-fraction against the butterfly peak measured on this GPU (hs_int_peak).
+fraction against the butterfly peak measured on this GPU (hs_int_peak for
+the integer butterflies of the 60-bit primes, hs_f64_peak for the FP64-pipe
+butterflies of the ~50-bit primes, mixed by the ModUp jobs' prime split).
 
 ``--impl reference`` times the reference algorithm on the host CPU instead:
 the CPU oracle (oracle/, a C restatement of the reference path, bit-exact,
@@ -321,6 +323,35 @@ def int_peak(q: int) -> dict:
     return {"butterflies_per_s": out[0], "imad_per_s": out[1], "iadd_per_s": out[2], "sms": int(out[3])}
 
 
+F64_MAX_Q = (1 << 50) + (1 << 40)      # primes whose forward butterflies run on the FP64 pipe (ntt.cuh)
+
+
+def f64_peak(q: int) -> dict | None:
+    import ctypes
+    from paper_2604_11659_b200 import device as D
+    from paper_2604_11659_b200._lib import check, lib
+    if q > F64_MAX_Q:
+        return None
+    out = (ctypes.c_double * 4)()
+    check(lib().hs_f64_peak(int(q), out, D.stream()))
+    return {"butterflies_per_s": out[0], "dfma_per_s": out[1]}
+
+
+def modup_peak(params, ipk: dict, fpk: dict | None) -> dict:
+    """Butterfly peak of the ModUp NTTs at the top level: digit i lifted to
+    every modulus m != i of the chain and the aux prime; targets <= F64_MAX_Q
+    run the FP64-pipe butterflies, the others the integer ones.  Mixed peak =
+    1 / (rho / P_int + (1 - rho) / P_f64), rho = integer share of the jobs."""
+    primes = [*params.modulus_chain, params.aux_prime]
+    L = params.levels
+    jobs = [(i, m) for i in range(L + 1) for m in list(range(L + 1)) + [L + 1] if m != i]
+    rho = sum(primes[m] > F64_MAX_Q for _, m in jobs) / len(jobs)
+    if fpk is None:
+        rho = 1.0
+    pk = 1.0 / (rho / ipk["butterflies_per_s"] + ((1.0 - rho) / fpk["butterflies_per_s"] if fpk else 0.0))
+    return {"butterflies_per_s": pk, "integer_job_share": round(rho, 4)}
+
+
 def roofline_entry(kind: int, rec: dict, peaks: dict, ipk: dict | None, workload: str,
                    step_ms_total: float) -> dict:
     peak = peaks.get("hbm_gbs", 6650.0)
@@ -344,8 +375,11 @@ def roofline_entry(kind: int, rec: dict, peaks: dict, ipk: dict | None, workload
         bps = rec["work"] / (rec["ms"] * 1e-3) if rec["ms"] else 0.0
         e["int_pipe"] = {"achieved": round(bps / 1e9, 2), "peak": round(ipk["butterflies_per_s"] / 1e9, 2),
                          "unit": "G butterflies/s", "frac": round(bps / ipk["butterflies_per_s"], 4),
-                         "peak_source": "hs_int_peak: the engine's forward butterfly on "
-                                        "register-resident data, measured on this GPU"}
+                         "integer_job_share": ipk.get("integer_job_share"),
+                         "peak_source": "hs_int_peak / hs_f64_peak: the engine's forward butterflies "
+                                        "(integer Shoup for the 60-bit primes, FP64 pipe for the "
+                                        "~50-bit ones) on register-resident data, measured on this "
+                                        "GPU, mixed by the ModUp jobs' prime split at the top level"}
     elif kind == PROBE_KS_INNER:
         e["int_pipe"] = {"achieved": round(rec["work"] / (rec["ms"] * 1e-3) / 1e9, 2) if rec["ms"] else 0.0,
                          "unit": "G 64x64->128-bit MACs/s"}
@@ -549,7 +583,12 @@ def run_b200_arm(args, wl):
     ks_floor = None
     if rank == 0:
         ipk = int_peak(params.modulus_chain[1])
-        ents = {k: roofline_entry(k, probes[k], peaks, ipk, args.workload, dev_ms) for k in probes}
+        fpk = f64_peak(params.modulus_chain[1])
+        if fpk:
+            ipk["f64_butterflies_per_s"] = fpk["butterflies_per_s"]
+            ipk["dfma_per_s"] = fpk["dfma_per_s"]
+        mpk = modup_peak(params, ipk, fpk)
+        ents = {k: roofline_entry(k, probes[k], peaks, mpk, args.workload, dev_ms) for k in probes}
         top = max(ents, key=lambda k: probes[k]["ms"])
         roof = ents[top]
         other = ents[PROBE_KS_INNER if top == PROBE_MODUP else PROBE_MODUP]

@@ -74,6 +74,9 @@ int64_t hs_launch_count(void);
 hs_status hs_probe_arm(int32_t mask);
 hs_status hs_probe_read(int32_t kind, double* out4);
 hs_status hs_int_peak(uint64_t q, double* out4, void* stream);
+/* hs_f64_peak(q, out4, stream): the FP64-pipe forward butterflies used for
+ * primes q <= 2^50 + 2^40, measured the same way: {butterflies/s, DFMA/s, 0, SMs}. */
+hs_status hs_f64_peak(uint64_t q, double* out4, void* stream);
 
 /* ---------------------------------------------------------------- context
  * Replaces CkksContext.__init__ precomputation (ckks/context.py:31-58) and

@@ -38,6 +38,7 @@ _SIGS = {
     "hs_probe_arm": (ctypes.c_int, [ctypes.c_int32]),
     "hs_probe_read": (ctypes.c_int, [ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]),
     "hs_int_peak": (ctypes.c_int, [ctypes.c_uint64, ctypes.POINTER(ctypes.c_double), c_vp]),
+    "hs_f64_peak": (ctypes.c_int, [ctypes.c_uint64, ctypes.POINTER(ctypes.c_double), c_vp]),
     "hs_ctx_create": (ctypes.c_int, [ctypes.POINTER(c_vp), ctypes.c_int, ctypes.c_uint32,
                                      ctypes.c_uint32, c_u64p, ctypes.c_uint64]),
     "hs_ctx_destroy": (None, [c_vp]),

@@ -7,7 +7,9 @@
 //      - butterflies/s of the NTT engine's own forward butterfly
 //        (unit_butterflies, approximate-quotient Shoup, lazy reduction
 //        schedule) on register-resident data, radix-16 units, full occupancy;
-//      - IMAD/s (mad.wide.u32 chains, FMA pipe) and IADD3/s (ALU pipe).
+//      - IMAD/s (mad.wide.u32 chains, FMA pipe) and IADD3/s (ALU pipe);
+//  * hs_f64_peak: the same for the FP64-pipe butterflies (ntt.cuh
+//    unit_butterflies_f64) and DFMA/s.
 #include <vector>
 
 #include "ops.cuh"
@@ -42,6 +44,43 @@ __global__ void __launch_bounds__(PK_T, MINB) bfly_peak_kernel(PrimeConst P, con
 #pragma unroll
     for (int e = 0; e < 16; e++) acc ^= v[e];
     if (acc == 0x123456789abcdefull) sink[0] = acc;    // never true in practice; keeps the work live
+}
+
+// The FP64-pipe forward butterflies (unit_butterflies_f64, ~50-bit primes)
+// on 16 register values, same shape as bfly_peak_kernel.
+template <int MINB>
+__global__ void __launch_bounds__(PK_T, MINB) bfly_f64_peak_kernel(double q, double qinv, const double2* tw_g,
+                                                                   int iters, u64* sink) {
+    __shared__ double2 tw[64];
+    if (threadIdx.x < 64) tw[threadIdx.x] = tw_g[threadIdx.x];
+    __syncthreads();
+    u64 v[16];
+#pragma unroll
+    for (int e = 0; e < 16; e++)
+        v[e] = (u64)__double_as_longlong((double)(((int)threadIdx.x << 12) + e - (int)blockIdx.x));
+    const u32 Y = 1u + (threadIdx.x & 1u);
+#pragma unroll 1
+    for (int it = 0; it < iters; it++) unit_butterflies_f64<4, 3>(v, tw, Y, q, qinv);   // reduces at 3 and 5
+    u64 acc = 0;
+#pragma unroll
+    for (int e = 0; e < 16; e++) acc ^= v[e];
+    if (acc == 0x123456789abcdefull) sink[0] = acc;
+}
+
+// 8 independent DFMA chains per thread (FP64 pipe).
+__global__ void __launch_bounds__(PK_T, PK_MINB) dfma_peak_kernel(int iters, u64* sink) {
+    double a[8];
+    const double m = 0.999999 + threadIdx.x * 1e-12, c = 1e-9;
+#pragma unroll
+    for (int k = 0; k < 8; k++) a[k] = threadIdx.x + k;
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int k = 0; k < 8; k++) a[k] = __fma_rn(a[k], m, c);
+    }
+    double x = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) x += a[k];
+    if (x == 1234.5) sink[0] = 1;
 }
 
 // 8 independent mad.wide.u32 chains per thread (FMA pipe).
@@ -161,6 +200,66 @@ hs_status hs_int_peak(uint64_t q, double* out, void* stream) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         set_error(std::string("int peak probe failed: ") + cudaGetErrorString(e));
+        return HS_CUDA_ERROR;
+    }
+    return HS_OK;
+}
+
+// out[0] = FP64-path butterflies/s (prime q, which must be <= 2^50 + 2^40),
+// out[1] = DFMA/s, out[2] = 0, out[3] = SM count.
+hs_status hs_f64_peak(uint64_t q, double* out, void* stream) {
+    if (q > (1ull << 50) + (1ull << 40)) {
+        set_error("hs_f64_peak: the FP64 butterflies need q <= 2^50 + 2^40");
+        return HS_PARAMETER_ERROR;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    int dev = 0, nsm = 0;
+    HS_CUDA(cudaGetDevice(&dev));
+    HS_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    std::vector<double2> tw(64);
+    u64 w = 3;
+    for (int k = 0; k < 64; k++) {
+        w = (u64)((unsigned __int128)w * 0x9e3779b97f4a7c15ull % q);
+        tw[k] = make_double2((double)w, (double)w / (double)q);
+    }
+    double2* d_tw = nullptr;
+    u64* d_sink = nullptr;
+    HS_CUDA(cudaMalloc(&d_tw, 64 * sizeof(double2)));
+    HS_CUDA(cudaMalloc(&d_sink, 8));
+    HS_CUDA(cudaMemcpy(d_tw, tw.data(), 64 * sizeof(double2), cudaMemcpyHostToDevice));
+    const int grid = nsm * PK_MINB * 4;
+    cudaEvent_t e0, e1;
+    HS_CUDA(cudaEventCreate(&e0));
+    HS_CUDA(cudaEventCreate(&e1));
+    auto timed = [&](auto launch) -> double {
+        launch();
+        cudaEventRecord(e0, st);
+        for (int r = 0; r < 3; r++) launch();
+        cudaEventRecord(e1, st);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        return ms / 3.0;
+    };
+    const int ib = 512, ii = 4096;
+    const double qd = (double)q, qinv = 1.0 / qd;
+    const double ms_b8 = timed([&] { bfly_f64_peak_kernel<8><<<grid, PK_T, 0, st>>>(qd, qinv, d_tw, ib, d_sink); });
+    const double ms_b4 = timed([&] { bfly_f64_peak_kernel<4><<<grid, PK_T, 0, st>>>(qd, qinv, d_tw, ib, d_sink); });
+    const double ms_b = ms_b8 < ms_b4 ? ms_b8 : ms_b4;
+    const double ms_f = timed([&] { dfma_peak_kernel<<<grid, PK_T, 0, st>>>(ii, d_sink); });
+    note_launch(12);
+    const double threads = (double)grid * PK_T;
+    out[0] = threads * ib * 32.0 / (ms_b * 1e-3);
+    out[1] = threads * ii * 8.0 / (ms_f * 1e-3);
+    out[2] = 0.0;
+    out[3] = nsm;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(d_tw);
+    cudaFree(d_sink);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error(std::string("f64 peak probe failed: ") + cudaGetErrorString(e));
         return HS_CUDA_ERROR;
     }
     return HS_OK;
