@@ -159,10 +159,10 @@ hs_status hs_ctx_create(hs_ctx** out, int device, uint32_t n, uint32_t levels,
     }
     // per-prime constants and twiddles
     std::vector<ulonglong2> tw((size_t)P * n), itw((size_t)P * n);
-    std::vector<double2> twd((size_t)P * n);
+    std::vector<double2> twd((size_t)P * n), itwd((size_t)P * n);
     std::vector<u64> pw(n), ipw(n);
     c->pc.resize(P);
-    // Forward NTT butterflies on the FP64 pipe for primes <= 2^50 + 2^40 (every
+    // NTT butterflies (both directions) on the FP64 pipe for primes <= 2^50 + 2^40 (every
     // scaling prime of a scale_bits <= 50 chain; ntt.cuh unit_butterflies_f64
     // states the bounds).  HS_NTT_F64=0 keeps every prime on the integer path.
     const char* f64env = getenv("HS_NTT_F64");
@@ -190,6 +190,7 @@ hs_status hs_ctx_create(hs_ctx** out, int device, uint32_t n, uint32_t levels,
             tw[(size_t)p * n + i] = shoup_pair(pw[r], q);
             // w < 2^51 is exact in a double; RN(w / q) by one IEEE division of exact operands
             twd[(size_t)p * n + i] = make_double2((double)pw[r], (double)pw[r] / (double)q);
+            itwd[(size_t)p * n + i] = make_double2((double)ipw[r], (double)ipw[r] / (double)q);
             itw[(size_t)p * n + i] = shoup_pair(ipw[r], q);
         }
     }
@@ -225,7 +226,8 @@ hs_status hs_ctx_create(hs_ctx** out, int device, uint32_t n, uint32_t levels,
     size_t off_ql = off_ai + auxinv.size() * sizeof(ulonglong2);
     size_t off_twd = off_ql + qlinv.size() * sizeof(ulonglong2);
     off_twd = (off_twd + 255) & ~(size_t)255;
-    size_t total = off_twd + twd.size() * sizeof(double2);
+    size_t off_itwd = off_twd + twd.size() * sizeof(double2);
+    size_t total = off_itwd + itwd.size() * sizeof(double2);
     cudaError_t e = cudaMalloc(&c->d_blob, total);
     if (e != cudaSuccess) {
         set_error(std::string("cudaMalloc tables: ") + cudaGetErrorString(e));
@@ -239,7 +241,8 @@ hs_status hs_ctx_create(hs_ctx** out, int device, uint32_t n, uint32_t levels,
     cudaMemcpy(base + off_df, df.data(), df.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice);
     cudaMemcpy(base + off_ai, auxinv.data(), auxinv.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice);
     cudaMemcpy(base + off_ql, qlinv.data(), qlinv.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice);
-    e = cudaMemcpy(base + off_twd, twd.data(), twd.size() * sizeof(double2), cudaMemcpyHostToDevice);
+    cudaMemcpy(base + off_twd, twd.data(), twd.size() * sizeof(double2), cudaMemcpyHostToDevice);
+    e = cudaMemcpy(base + off_itwd, itwd.data(), itwd.size() * sizeof(double2), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
         set_error(std::string("table upload: ") + cudaGetErrorString(e));
         cudaFree(c->d_blob);
@@ -259,6 +262,7 @@ hs_status hs_ctx_create(hs_ctx** out, int device, uint32_t n, uint32_t levels,
     d.auxinv = (const ulonglong2*)(base + off_ai);
     d.qlinv = (const ulonglong2*)(base + off_ql);
     d.twd = (const double2*)(base + off_twd);
+    d.itwd = (const double2*)(base + off_itwd);
     *out = c;
     return (hs_status)HS_OK;
 }

@@ -22,6 +22,7 @@ struct Dev {
     const ulonglong2* itw;       // inverse roots
     const double2* twd;          // [(L+2) * n] {w, RN(w / q)} forward roots as doubles
                                  // (primes with PrimeConst::pad & PC_F64; ntt.cuh FP64 butterflies)
+    const double2* itwd;         // inverse roots as doubles
     const ulonglong2* df;        // [L+1] digit factor (Q_L/q_i)^-1 mod q_i, Shoup pair
     const ulonglong2* dfR;       // [L+1] the same times 2^64 mod q_i
     const ulonglong2* auxinv;    // [L+1] p^-1 mod q_m

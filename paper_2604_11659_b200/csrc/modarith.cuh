@@ -25,7 +25,7 @@ struct PrimeConst {
     u64 m64;         // floor(2^64 / q): generic 64-bit Barrett (reduce64)
     u64 r_sh;        // floor(r_mod 2^64 / q): Shoup companion of 2^64 mod q
     u32 k;           // bitlen(q)
-    u32 pad;         // flags: PC_F64 = forward NTT butterflies on the FP64 pipe (q <= 2^50 + 2^40)
+    u32 pad;         // flags: PC_F64 = NTT butterflies on the FP64 pipe (q <= 2^50 + 2^40)
 };
 #define PC_F64 1u
 

@@ -344,6 +344,9 @@ HS_DEV void unit_butterflies(u64* v, const ulonglong2* __restrict__ tw, u32 Y, u
 // Passes hand raw doubles to each other.  Any other prime (the 60-bit first
 // and auxiliary primes) stays on the integer path.
 HS_DEV constexpr bool f64_reduce_at(int gs) { return gs & 1; }
+#ifndef HS_NTT_F64_INV
+#define HS_NTT_F64_INV 1           // inverse NTTs on the FP64 pipe too
+#endif
 constexpr double kF64Magic = 6755399441055744.0;   // 1.5 * 2^52
 
 HS_DEV double f64_rint_mul(double a, double b) {
@@ -379,11 +382,35 @@ HS_DEV void unit_butterflies_f64(u64* v, const double2* __restrict__ tw, u32 Y, 
     }
 }
 
-// u64 in [0, 4q) -> reduced double bits, |x| <= q/2 (first forward pass)
+// Inverse (Gentleman-Sande) butterflies on the FP64 pipe: x' = rint-reduce(x + y)
+// (|x'| <= q/2 + tiny), y' = (x - y) w mod q (lazy).  Every value stays below
+// B = 1/2 + k 2B, i.e. 0.67q (k <= 0.1252), and |x - y| <= 1.34q keeps the
+// rint argument below 2^51.
+template <int R>
+HS_DEV void unit_butterflies_f64_inv(u64* v, const double2* __restrict__ tw, u32 Y, double q, double qinv) {
+    constexpr int NU = 1 << R;
+#pragma unroll
+    for (int jj = 0; jj < R; jj++) {
+        const int j = R - 1 - jj;
+        const double2* __restrict__ twp = tw + (Y << j);
+        const int bit = 1 << (R - 1 - j);
+#pragma unroll
+        for (int e = 0; e < NU; e++) {
+            if (e & bit) continue;
+            const double2 w = twp[e >> (R - j)];
+            const double x = __longlong_as_double((long long)v[e]);
+            const double y = __longlong_as_double((long long)v[e + bit]);
+            v[e] = (u64)__double_as_longlong(f64_reduce(__dadd_rn(x, y), q, qinv));
+            v[e + bit] = (u64)__double_as_longlong(f64_mulmod(__dsub_rn(x, y), w.x, w.y, q));
+        }
+    }
+}
+
+// u64 in [0, 4q) -> reduced double bits, |x| <= q/2 (first pass)
 HS_DEV u64 f64_enter(u64 u, double q, double qinv) {
     return (u64)__double_as_longlong(f64_reduce(__ull2double_rn(u), q, qinv));
 }
-// double bits, |x| < 2^52.5 -> u64 in [q/2, 3q/2] (last forward pass):
+// double bits, |x| < 2^52.5 -> u64 in [q/2, 3q/2] (last pass):
 // x - q rint(x/q) + q + 2^52 lies in [2^52, 2^53), whose mantissa is the value
 HS_DEV u64 f64_leave(u64 bits, double q, double qinv, double q_plus_2p52) {
     const double r = __dadd_rn(f64_reduce(__longlong_as_double((long long)bits), q, qinv), q_plus_2p52);
@@ -442,10 +469,10 @@ struct PassEngine {
         typename Job::Ctx jc;
         PrimeConst P;
         const ulonglong2* __restrict__ tw;
-        const double2* __restrict__ twd;   // FP64 forward roots (f64)
+        const double2* __restrict__ twd;   // FP64 roots of the pass's direction (f64)
         u32 t, hi0, lo0;
         u64 nq, four_q;
-        bool f64;                          // forward pass on the FP64 pipe (PC_F64)
+        bool f64;                          // butterflies on the FP64 pipe (PC_F64)
         double qd, qinvd;
         HS_DEV u32 gidx(u32 h, u32 g, u32 c) const {
             return ((hi0 + h) << (LOGN - S0)) | (g << LO_BITS) | (lo0 + c);
@@ -497,9 +524,10 @@ struct PassEngine {
             for (int k = 0; k < 2; k++) {
                 const auto u = M::unit(E.t + k * T);
                 const u32 Y = (((1u << S0) + E.hi0 + u.h) << M::AA) + u.gh;
-                if (FWD && E.f64)
-                    unit_butterflies_f64<M::RR, S0 + M::AA>(v, E.twd, Y, E.qd, E.qinvd);
-                else
+                if (E.f64) {
+                    if constexpr (FWD) unit_butterflies_f64<M::RR, S0 + M::AA>(v, E.twd, Y, E.qd, E.qinvd);
+                    else unit_butterflies_f64_inv<M::RR>(v, E.twd, Y, E.qd, E.qinvd);
+                } else
                     unit_butterflies<FWD, M::RR, S0 + M::AA>(v, E.tw, Y, E.nq, E.P.two_q, E.four_q);
 #pragma unroll
                 for (int e = 0; e < M::NU; e++) {
@@ -513,17 +541,18 @@ struct PassEngine {
             for (int k = 0; k < M::UPT; k++) {
                 const auto u = M::unit(E.t + k * T);
                 const u32 Y = (((1u << S0) + E.hi0 + u.h) << M::AA) + u.gh;
-                if (FWD && E.f64)
-                    unit_butterflies_f64<M::RR, S0 + M::AA>(v + k * M::NU, E.twd, Y, E.qd, E.qinvd);
-                else
+                if (E.f64) {
+                    if constexpr (FWD) unit_butterflies_f64<M::RR, S0 + M::AA>(v + k * M::NU, E.twd, Y, E.qd, E.qinvd);
+                    else unit_butterflies_f64_inv<M::RR>(v + k * M::NU, E.twd, Y, E.qd, E.qinvd);
+                } else
                     unit_butterflies<FWD, M::RR, S0 + M::AA>(v + k * M::NU, E.tw, Y, E.nq, E.P.two_q, E.four_q);
             }
         }
     }
-    // FP64 forward path: enter after the first pass's load, leave before the
-    // last pass's store (passes in between exchange raw doubles)
+    // FP64 path: enter after the first pass's load, leave before the last
+    // pass's store (passes in between exchange raw doubles)
     HS_DEV static void f64_in(u64* v, const Env& E) {
-        if constexpr (FWD && FIRST) {
+        if constexpr (FIRST) {
             if (E.f64) {
 #pragma unroll
                 for (int k = 0; k < EPT; k++) v[k] = f64_enter(v[k], E.qd, E.qinvd);
@@ -531,7 +560,7 @@ struct PassEngine {
         }
     }
     HS_DEV static void f64_out(u64* v, const Env& E) {
-        if constexpr (FWD && LAST) {
+        if constexpr (LAST) {
             if (E.f64) {
                 const double k = E.qd + 4503599627370496.0;   // q + 2^52
 #pragma unroll
@@ -633,12 +662,10 @@ ntt_pass_kernel(Dev d, Job job, int jbase) {
     E.t = threadIdx.x;
     E.nq = 0ull - E.P.q;
     E.four_q = E.P.two_q << 1;
-    E.f64 = FWD && (E.P.pad & PC_F64);
-    if (FWD) {
-        E.twd = d.twd + ((size_t)p << LOGN);
-        E.qd = (double)E.P.q;
-        E.qinvd = __drcp_rn(E.qd);
-    }
+    E.f64 = (E.P.pad & PC_F64) && (FWD || HS_NTT_F64_INV);
+    E.twd = (FWD ? d.twd : d.itwd) + ((size_t)p << LOGN);
+    E.qd = (double)E.P.q;
+    E.qinvd = __drcp_rn(E.qd);
     // One code path for every prime: a lazy forward variant (no upper-input
     // reduction for sub-2^56 primes) saved ~5 instructions per butterfly but
     // doubled the kernel's code, and instruction-cache misses cost more than

@@ -1,6 +1,6 @@
-"""CPU model of the FP64-pipe forward butterflies (csrc/ntt.cuh,
-unit_butterflies_f64 / f64_enter / f64_leave), checked against an exact
-integer NTT.
+"""CPU model of the FP64-pipe NTT butterflies (csrc/ntt.cuh,
+unit_butterflies_f64 / unit_butterflies_f64_inv / f64_enter / f64_leave),
+checked against exact integer transforms.
 
 Every double operation of the device code is emulated with IEEE round-to-
 nearest-even semantics (Python float arithmetic for mul/add/sub, an exact
@@ -138,6 +138,75 @@ def model_ntt(a, q, roots):
         assert q // 2 - 2 <= u <= 3 * q // 2 + 2          # [q/2, 3q/2] handed to the epilogue
         out.append(u % q)
     return out
+
+
+def exact_gs(a, q, iroots):
+    """Gentleman-Sande stages of the inverse NTT (without the n^-1 factor,
+    which the device applies in the job's epilogue)."""
+    a = list(a)
+    n = len(a)
+    t, m = 1, n
+    while m > 1:
+        h = m // 2
+        j1 = 0
+        for i in range(h):
+            w = iroots[h + i]
+            for j in range(j1, j1 + t):
+                u, v = a[j], a[j + t]
+                a[j], a[j + t] = (u + v) % q, (u - v) * w % q
+            j1 += 2 * t
+        t *= 2
+        m = h
+    return a
+
+
+def model_gs(a, q, iroots):
+    """unit_butterflies_f64_inv: x' = reduce(x + y), y' = (x - y) w mod q."""
+    qd = float(q)
+    qinv = float(Fraction(1, q))
+    x = [reduce(float(v), qd, qinv) for v in a]
+    n = len(x)
+    bound = 0.0
+    t, m = 1, n
+    while m > 1:
+        h = m // 2
+        j1 = 0
+        for i in range(h):
+            w = iroots[h + i]
+            wd, wq = float(w), float(w) / qd
+            for j in range(j1, j1 + t):
+                u, v = x[j], x[j + t]
+                x[j] = reduce(u + v, qd, qinv)
+                x[j + t] = mulmod(u - v, wd, wq, qd)
+                bound = max(bound, abs(x[j]), abs(x[j + t]))
+            j1 += 2 * t
+        t *= 2
+        m = h
+    assert bound <= 0.7 * q, bound / q
+    out = []
+    for v in x:
+        r = reduce(v, qd, qinv) + (qd + 2.0 ** 52)
+        u = int(r) - 2 ** 52
+        assert q // 2 - 2 <= u <= 3 * q // 2 + 2
+        out.append(u % q)
+    return out
+
+
+@pytest.mark.parametrize("kind", ["random", "max", "alternating"])
+def test_f64_inverse_gs_model_is_exact(kind):
+    n, logn = 2048, 11
+    q = ntt_prime(n)
+    ipsi = pow(psi_of(q, n), q - 2, q)
+    ipw = [pow(ipsi, k, q) for k in range(n)]
+    iroots = [ipw[brev(i, logn)] for i in range(n)]
+    rng = np.random.default_rng(11)
+    if kind == "random":
+        a = [int(v) for v in rng.integers(0, 4 * q, n, dtype=np.uint64)]
+    elif kind == "max":
+        a = [4 * q - 1] * n
+    else:
+        a = [(4 * q - 1) if k & 1 else 0 for k in range(n)]
+    assert model_gs(a, q, iroots) == exact_gs([v % q for v in a], q, iroots)
 
 
 @pytest.mark.parametrize("kind", ["random", "max", "alternating"])
