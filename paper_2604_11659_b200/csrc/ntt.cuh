@@ -323,7 +323,8 @@ HS_DEV void unit_butterflies(u64* v, const ulonglong2* __restrict__ tw, u32 Y, u
     }
 }
 
-// ---- forward butterflies on the FP64 pipe (primes q <= 2^50 + 2^40, PC_F64)
+// ---- NTT butterflies on the FP64 pipe (primes q <= 2^50 + 2^40, PC_F64);
+// forward (Cooley-Tukey) here, inverse (Gentleman-Sande) in unit_butterflies_f64_inv
 // The Shoup products above are 64-bit multiplies (IMAD.WIDE / IMAD.HI) that
 // keep the FMA-heavy pipe ~80% busy; B200 also has a full-rate FP64 pipe, and
 // for ~50-bit primes a residue is an exact double.  Values are signed
